@@ -1,0 +1,178 @@
+"""Deterministic graph generators producing simple undirected graphs as CSR.
+
+Graph semantics follow PAPER.md:357 (A_G is a 0-1 symmetric CSR adjacency)
+and the reading in SURVEY.md §8(c) "Graph semantics": undirected, simple,
+duplicates removed, self-loops dropped, column ids sorted inside each row.
+
+* ``erdos_renyi``: G(n, m) with m uniform distinct pairs.
+* ``rmat``: RMAT(a,b,c,d) edge draw (Chakrabarti et al.), random
+  id permutation, symmetrised + deduplicated (SURVEY §8(d) D2–D5a).
+* small closed-form graphs (cycle, path, complete, "house+tail") used by the
+  oracle pins (SURVEY §8(c) "What pins each part").
+
+Everything is numpy with ``default_rng(seed)``; the random stream is fixed by
+(seed, chunking) so the same arrays come out on every machine.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+
+@dataclass
+class CSR:
+    """Symmetric 0-1 adjacency in CSR form: int64 row_offsets[n+1], int32 col[nnz]."""
+
+    n: int
+    row_offsets: np.ndarray
+    col_indices: np.ndarray
+    name: str = ""
+
+    @property
+    def nnz(self) -> int:
+        return int(self.col_indices.shape[0])
+
+    @property
+    def degrees(self) -> np.ndarray:
+        return np.diff(self.row_offsets)
+
+    def edges(self):
+        """Undirected edge list (u < v) as an (m, 2) int64 array."""
+        rows = np.repeat(np.arange(self.n, dtype=np.int64), self.degrees)
+        cols = self.col_indices.astype(np.int64)
+        keep = rows < cols
+        return np.stack([rows[keep], cols[keep]], axis=1)
+
+    def nbytes(self) -> int:
+        return self.row_offsets.nbytes + self.col_indices.nbytes
+
+
+def csr_from_edges(n: int, u, v, name: str = "") -> CSR:
+    """Symmetrise, drop self-loops, deduplicate, sort -> CSR."""
+    u = np.asarray(u, dtype=np.int64).ravel()
+    v = np.asarray(v, dtype=np.int64).ravel()
+    keep = u != v
+    u, v = u[keep], v[keep]
+    src = np.concatenate([u, v])
+    dst = np.concatenate([v, u])
+    keys = np.unique(src * np.int64(n) + dst)
+    src = keys // n
+    dst = keys - src * n
+    counts = np.bincount(src, minlength=n).astype(np.int64)
+    row_offsets = np.zeros(n + 1, dtype=np.int64)
+    np.cumsum(counts, out=row_offsets[1:])
+    return CSR(n=n, row_offsets=row_offsets, col_indices=dst.astype(np.int32), name=name)
+
+
+def erdos_renyi(n: int, m: int, seed: int = 1) -> CSR:
+    """G(n, m): m distinct undirected pairs drawn uniformly."""
+    rng = np.random.default_rng(seed)
+    if m > n * (n - 1) // 2:
+        raise ValueError("m exceeds the number of vertex pairs")
+    have = np.zeros(0, dtype=np.int64)
+    while have.shape[0] < m:
+        need = m - have.shape[0]
+        a = rng.integers(0, n, size=2 * need + 16, dtype=np.int64)
+        b = rng.integers(0, n, size=2 * need + 16, dtype=np.int64)
+        keep = a != b
+        lo = np.minimum(a[keep], b[keep])
+        hi = np.maximum(a[keep], b[keep])
+        keys = lo * n + hi
+        # keep first occurrences in draw order, then merge with what we have
+        _, first = np.unique(keys, return_index=True)
+        keys = keys[np.sort(first)]
+        keys = keys[~np.isin(keys, have)]
+        have = np.concatenate([have, keys[:need]])
+    lo, hi = have // n, have % n
+    return csr_from_edges(n, lo, hi, name=f"ER(n={n},m={m},seed={seed})")
+
+
+def rmat(scale: int, m: int, a: float, b: float, c: float, seed: int = 1,
+         perm_seed: int | None = 7, chunk: int = 1 << 24) -> CSR:
+    """RMAT(a,b,c,d=1-a-b-c) with m drawn directed edges over n = 2^scale vertices.
+
+    Each edge picks one quadrant per level (row bit set for quadrants c,d; column
+    bit set for b,d).  Vertex ids are then relabelled by a random permutation
+    (``perm_seed``) so degree is uncorrelated with id, then the edge set is
+    symmetrised and deduplicated (SURVEY §8(d) D4 recipe).
+    """
+    n = 1 << scale
+    rng = np.random.default_rng(seed)
+    us, vs = [], []
+    ab, abc = a + b, a + b + c
+    left = m
+    while left > 0:
+        cnt = min(chunk, left)
+        left -= cnt
+        u = np.zeros(cnt, dtype=np.int64)
+        v = np.zeros(cnt, dtype=np.int64)
+        for lvl in range(scale):
+            r = rng.random(cnt, dtype=np.float64)
+            bit = np.int64(1) << np.int64(scale - 1 - lvl)
+            row_bit = r >= ab
+            col_bit = ((r >= a) & (r < ab)) | (r >= abc)
+            u |= np.where(row_bit, bit, 0)
+            v |= np.where(col_bit, bit, 0)
+        us.append(u)
+        vs.append(v)
+    u = np.concatenate(us)
+    v = np.concatenate(vs)
+    if perm_seed is not None:
+        perm = np.random.default_rng(perm_seed).permutation(n).astype(np.int64)
+        u, v = perm[u], perm[v]
+    return csr_from_edges(n, u, v, name=f"RMAT(scale={scale},m={m},a={a},b={b},c={c},seed={seed})")
+
+
+def rmat_1m_like(scale: int = 20, edge_factor: float = 100.0, seed: int = 1) -> CSR:
+    """RMAT(0.45,0.22,0.22,0.11), scale 20, m = 1.05e8 drawn, perm seed 7.
+
+    ``edge_factor`` = drawn edges per vertex (1.05e8 / 2^20 ≈ 100.1).  Smaller
+    ``scale`` keeps the same recipe (used for parity-size cases).
+    """
+    m = int(round(1.05e8 * (1 << scale) / (1 << 20) * (edge_factor / 100.1354)))
+    g = rmat(scale, m, 0.45, 0.22, 0.22, seed=seed, perm_seed=7)
+    g.name = f"RMAT-1M-like(scale={scale},m={m},seed={seed})"
+    return g
+
+
+def cycle_graph(n: int) -> CSR:
+    i = np.arange(n)
+    return csr_from_edges(n, i, (i + 1) % n, name=f"C{n}")
+
+
+def path_graph(n: int) -> CSR:
+    i = np.arange(n - 1)
+    return csr_from_edges(n, i, i + 1, name=f"P{n}")
+
+
+def complete_graph(n: int) -> CSR:
+    u, v = np.triu_indices(n, 1)
+    return csr_from_edges(n, u, v, name=f"K{n}")
+
+
+def house_tail_graph() -> CSR:
+    """SURVEY §8(c) pin 3 end-to-end graph: n=8, 10 edges."""
+    e = [(0, 1), (1, 2), (2, 3), (3, 0), (0, 4), (1, 4), (3, 5), (5, 6), (6, 7), (2, 6)]
+    u, v = zip(*e)
+    return csr_from_edges(8, u, v, name="house+tail")
+
+
+def disjoint_union(g1: CSR, g2: CSR) -> CSR:
+    e1 = g1.edges()
+    e2 = g2.edges() + g1.n
+    e = np.concatenate([e1, e2])
+    return csr_from_edges(g1.n + g2.n, e[:, 0], e[:, 1], name=f"{g1.name}+{g2.name}")
+
+
+def degree_stats(g: CSR) -> dict:
+    d = g.degrees
+    return {
+        "n": g.n,
+        "nnz": g.nnz,
+        "avg_deg": float(g.nnz / max(g.n, 1)),
+        "max_deg": int(d.max()) if g.n else 0,
+        "p50": float(np.percentile(d, 50)) if g.n else 0.0,
+        "p99": float(np.percentile(d, 99)) if g.n else 0.0,
+        "isolated": int((d == 0).sum()),
+    }
