@@ -1,0 +1,440 @@
+// api.cpp — the C ABI of libsg2v.so (include/sg2v.h).  Argument checking,
+// handle ownership, plan cache, workspace, the per-colouring launch sequence of
+// Alg. 5 and the estimate of Alg. 1.
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "sg2v_internal.h"
+
+namespace sg2v {
+
+static thread_local std::string g_err;
+static thread_local sg2v_options g_opts;
+static thread_local bool g_opts_init = false;
+
+void set_error(const std::string &msg) { g_err = msg; }
+
+static sg2v_status cuda_fail(const char *what, int code) {
+    set_error(std::string(what) + ": " + cudaGetErrorString((cudaError_t)code));
+    return SG2V_ECUDA;
+}
+
+#define SG2V_CK(call)                                                   \
+    do {                                                                \
+        cudaError_t _e = (call);                                        \
+        if (_e != cudaSuccess) return cuda_fail(#call, (int)_e);        \
+    } while (0)
+
+Template::~Template() {
+    for (auto &kv : plans)
+        if (kv.second && kv.second->d_index) cudaFree(kv.second->d_index);
+}
+
+// ----------------------------------------------------------------- profiling
+struct ProfRec {
+    int cls;
+    cudaEvent_t a, b;
+    double bytes;
+};
+static std::mutex g_prof_mu;
+static bool g_prof_on = false;
+static std::vector<ProfRec> g_prof;
+static std::vector<cudaEvent_t> g_ev_pool;
+static thread_local cudaEvent_t g_pending = nullptr;
+
+static cudaEvent_t ev_get() {
+    if (!g_ev_pool.empty()) {
+        cudaEvent_t e = g_ev_pool.back();
+        g_ev_pool.pop_back();
+        return e;
+    }
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    return e;
+}
+
+void prof_begin(int, void *stream) {
+    if (!g_prof_on) return;
+    std::lock_guard<std::mutex> lk(g_prof_mu);
+    g_pending = ev_get();
+    cudaEventRecord(g_pending, (cudaStream_t)stream);
+}
+
+void prof_end(int cls, double bytes, void *stream) {
+    if (!g_prof_on || !g_pending) return;
+    std::lock_guard<std::mutex> lk(g_prof_mu);
+    cudaEvent_t b = ev_get();
+    cudaEventRecord(b, (cudaStream_t)stream);
+    g_prof.push_back({cls, g_pending, b, bytes});
+    g_pending = nullptr;
+}
+
+// ------------------------------------------------------------------- helpers
+static int resolve_device(int dev) {
+    if (dev >= 0) return dev;
+    int d = 0;
+    cudaGetDevice(&d);
+    return d;
+}
+
+static sg2v_status ensure_device(int dev) {
+    int count = 0;
+    cudaError_t e = cudaGetDeviceCount(&count);
+    if (e != cudaSuccess || count == 0) {
+        set_error("no CUDA device available (libsg2v has no CPU fallback)");
+        return SG2V_ECUDA;
+    }
+    if (dev >= count) { set_error("device ordinal out of range"); return SG2V_EINVAL; }
+    SG2V_CK(cudaSetDevice(dev));
+    int major = 0;
+    cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev);
+    if (major != 10) {
+        set_error("libsg2v is built for sm_100a (B200) only");
+        return SG2V_ECUDA;
+    }
+    return SG2V_OK;
+}
+
+// Plans are cached per (precision, n, nnz, device); the index tables are
+// uploaded lazily, so planning itself needs no GPU (host-only tests use it).
+static sg2v_status get_plan(int64_t n, int64_t nnz, int device, const Template &t, sg2v_precision prec,
+                            bool upload, Plan **out) {
+    auto key = std::make_tuple((int)prec, n, nnz, device);
+    auto &slot = const_cast<Template &>(t).plans[key];
+    if (!slot) {
+        std::unique_ptr<Plan> pl;
+        sg2v_status st = make_plan(t, n, nnz, prec, pl);
+        if (st != SG2V_OK) return st;
+        slot = std::move(pl);
+    }
+    if (upload && !slot->d_index) {
+        SG2V_CK(cudaMalloc(&slot->d_index, slot->index.size() * sizeof(int32_t)));
+        SG2V_CK(cudaMemcpy(slot->d_index, slot->index.data(), slot->index.size() * sizeof(int32_t),
+                           cudaMemcpyHostToDevice));
+    }
+    *out = slot.get();
+    return SG2V_OK;
+}
+
+}  // namespace sg2v
+
+using namespace sg2v;
+
+struct sg2v_graph : public sg2v::Graph {};
+struct sg2v_template : public sg2v::Template {};
+
+extern "C" {
+
+const char *sg2v_last_error(void) { return g_err.c_str(); }
+const char *sg2v_version(void) { return "sg2v 0.1 (sm_100a)"; }
+
+void sg2v_options_default(sg2v_options *o) {
+    if (!o) return;
+    std::memset(o, 0, sizeof(*o));
+    o->precision = SG2V_F32;
+    o->iter_offset = 0;
+    o->iter_stride = 1;
+    o->mode = 0;
+    o->device = -1;
+}
+
+sg2v_status sg2v_set_options(const sg2v_options *o) {
+    if (!o) { set_error("options is NULL"); return SG2V_EINVAL; }
+    if (o->mode != 0 || o->nccl_comm) { set_error("only mode 0 (replicas) is implemented"); return SG2V_EINVAL; }
+    g_opts = *o;
+    g_opts_init = true;
+    return SG2V_OK;
+}
+
+sg2v_status sg2v_graph_load_csr(int64_t n, const int64_t *row_offsets, const int32_t *col_indices, int64_t nnz,
+                                uint32_t flags, sg2v_graph **out) {
+    if (!out) { set_error("out is NULL"); return SG2V_EINVAL; }
+    *out = nullptr;
+    if (n < 0 || n >= (int64_t(1) << 31) || nnz < 0) { set_error("n or nnz out of range"); return SG2V_EINVAL; }
+    if (!row_offsets || (nnz > 0 && !col_indices)) { set_error("CSR arrays are NULL"); return SG2V_EINVAL; }
+    const bool dev_ptrs = flags & SG2V_GRAPH_DEVICE_PTRS;
+    if (!dev_ptrs) {
+        if (row_offsets[0] != 0 || row_offsets[n] != nnz) { set_error("row_offsets[0] != 0 or row_offsets[n] != nnz"); return SG2V_EINVAL; }
+    }
+    sg2v_options o;
+    if (g_opts_init) o = g_opts; else sg2v_options_default(&o);
+    int dev = resolve_device(o.device);
+    sg2v_status st = ensure_device(dev);
+    if (st != SG2V_OK) return st;
+    auto *g = new sg2v_graph();
+    g->n = n;
+    g->nnz = nnz;
+    g->device = dev;
+    cudaStream_t s = (cudaStream_t)o.stream;
+    auto fail = [&](sg2v_status code) { sg2v_graph_free(g); return code; };
+    cudaError_t e;
+    if ((e = cudaMalloc(&g->d_rowptr, (n + 1) * sizeof(int64_t))) != cudaSuccess) return fail(cuda_fail("cudaMalloc rowptr", e));
+    if ((e = cudaMalloc(&g->d_col, std::max<int64_t>(nnz, 1) * sizeof(int32_t))) != cudaSuccess) return fail(cuda_fail("cudaMalloc col", e));
+    if ((e = cudaMalloc(&g->d_order, std::max<int64_t>(n, 1) * sizeof(int32_t))) != cudaSuccess) return fail(cuda_fail("cudaMalloc order", e));
+    cudaMemcpyKind kind = dev_ptrs ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+    if ((e = cudaMemcpyAsync(g->d_rowptr, row_offsets, (n + 1) * sizeof(int64_t), kind, s)) != cudaSuccess) return fail(cuda_fail("copy rowptr", e));
+    if (nnz > 0 && (e = cudaMemcpyAsync(g->d_col, col_indices, nnz * sizeof(int32_t), kind, s)) != cudaSuccess) return fail(cuda_fail("copy col", e));
+    if (dev_ptrs) {
+        int64_t ends[2];
+        cudaMemcpyAsync(&ends[0], g->d_rowptr, sizeof(int64_t), cudaMemcpyDeviceToHost, s);
+        cudaMemcpyAsync(&ends[1], g->d_rowptr + n, sizeof(int64_t), cudaMemcpyDeviceToHost, s);
+        if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return fail(cuda_fail("sync", e));
+        if (ends[0] != 0 || ends[1] != nnz) { set_error("row_offsets[0] != 0 or row_offsets[n] != nnz"); return fail(SG2V_EINVAL); }
+    }
+    if (flags & SG2V_GRAPH_VALIDATE) {
+        int bad = 0;
+        int rc = graph_validate(*g, &bad, s);
+        if (rc) return fail(cuda_fail("validate", rc));
+        if (bad) {
+            std::string m = "invalid CSR:";
+            if (bad & 1) m += " bad row_offsets;";
+            if (bad & 2) m += " column id out of range;";
+            if (bad & 4) m += " self-loop;";
+            if (bad & 8) m += " row not strictly sorted (unsorted or duplicate);";
+            if (bad & 16) m += " not symmetric;";
+            set_error(m);
+            return fail(SG2V_EINVAL);
+        }
+    }
+    int rc = graph_build_order(*g, s);
+    if (rc) return fail(cuda_fail("degree order", rc));
+    *out = g;
+    return SG2V_OK;
+}
+
+void sg2v_graph_free(sg2v_graph *g) {
+    if (!g) return;
+    int cur = 0;
+    cudaGetDevice(&cur);
+    cudaSetDevice(g->device);
+    cudaFree(g->d_rowptr);
+    cudaFree(g->d_col);
+    cudaFree(g->d_order);
+    cudaSetDevice(cur);
+    delete g;
+}
+
+sg2v_status sg2v_template_build(int32_t k, const int32_t *edges, int32_t root_hint, sg2v_template **out) {
+    if (!out) { set_error("out is NULL"); return SG2V_EINVAL; }
+    *out = nullptr;
+    if (k < 1 || k > 31) { set_error("k must be in [1, 31]"); return SG2V_EINVAL; }
+    if (root_hint < -1 || root_hint >= k) { set_error("root_hint out of range"); return SG2V_EINVAL; }
+    auto *t = new sg2v_template();
+    sg2v_status st = validate_template(k, edges, *t);
+    if (st != SG2V_OK) { delete t; return st; }
+    t->root_hint = root_hint;
+    t->alpha = automorphisms(*t);
+    double P = 1.0;
+    for (int i = 1; i <= k; ++i) P *= (double)i / (double)k;   // k!/k^k
+    t->P = P;
+    *out = t;
+    return SG2V_OK;
+}
+
+void sg2v_template_free(sg2v_template *t) { delete t; }
+
+sg2v_status sg2v_template_info(const sg2v_template *t, int32_t *k, double *alpha, double *P) {
+    if (!t) { set_error("template is NULL"); return SG2V_EINVAL; }
+    if (k) *k = t->k;
+    if (alpha) *alpha = t->alpha;
+    if (P) *P = t->P;
+    return SG2V_OK;
+}
+
+sg2v_status sg2v_workspace_bytes(const sg2v_graph *g, const sg2v_template *t, sg2v_precision prec, uint64_t *bytes) {
+    if (!g || !t || !bytes) { set_error("NULL argument"); return SG2V_EINVAL; }
+    if (prec < SG2V_F32 || prec > SG2V_U64) { set_error("bad precision"); return SG2V_EINVAL; }
+    if (t->k == 1 || g->n == 0) { *bytes = 0; return SG2V_OK; }
+    Plan *pl = nullptr;
+    sg2v_status st = get_plan(g->n, g->nnz, g->device, *t, prec, false, &pl);
+    if (st != SG2V_OK) return st;
+    *bytes = (uint64_t)pl->ws_bytes;
+    return SG2V_OK;
+}
+
+sg2v_status sg2v_plan_describe(const sg2v_graph *g, const sg2v_template *t, sg2v_precision prec, char *buf,
+                               uint64_t buf_len, uint64_t *needed) {
+    if (!g) { set_error("NULL argument"); return SG2V_EINVAL; }
+    return sg2v_plan_describe_n(g->n, g->nnz, t, prec, buf, buf_len, needed);
+}
+
+sg2v_status sg2v_plan_describe_n(int64_t n, int64_t nnz, const sg2v_template *t, sg2v_precision prec, char *buf,
+                                 uint64_t buf_len, uint64_t *needed) {
+    if (!t || n < 0 || nnz < 0) { set_error("bad argument"); return SG2V_EINVAL; }
+    if (prec < SG2V_F32 || prec > SG2V_U64) { set_error("bad precision"); return SG2V_EINVAL; }
+    std::string s;
+    if (t->k == 1 || n == 0) {
+        s = "{\"k\":" + std::to_string(t->k) + ",\"steps\":[],\"workspace_bytes\":0,\"alg_bytes\":0}";
+    } else {
+        Plan *pl = nullptr;
+        sg2v_status st = get_plan(n, nnz, -1, *t, prec, false, &pl);
+        if (st != SG2V_OK) return st;
+        s = pl->describe();
+    }
+    if (needed) *needed = s.size() + 1;
+    if (buf && buf_len > 0) {
+        size_t m = std::min<size_t>(s.size(), buf_len - 1);
+        std::memcpy(buf, s.data(), m);
+        buf[m] = 0;
+    }
+    return SG2V_OK;
+}
+
+sg2v_status sg2v_colorize(uint64_t seed, int64_t j, int64_t n, int32_t k, uint8_t *colors_out, void *stream) {
+    if (n < 0 || k < 1 || k > 31 || (n > 0 && !colors_out)) { set_error("bad argument"); return SG2V_EINVAL; }
+    int rc = launch_colorize(seed, j, n, k, colors_out, stream);
+    if (rc) return cuda_fail("colorize", rc);
+    return SG2V_OK;
+}
+
+sg2v_status sg2v_count_ex(const sg2v_graph *g, const sg2v_template *t, int32_t k, int64_t n_iter, uint64_t seed,
+                          const sg2v_options *op, double *estimate_out, double *colorful_out,
+                          uint64_t *colorful_u64_out) {
+    if (!g || !t) { set_error("graph or template is NULL"); return SG2V_EINVAL; }
+    if (k != t->k) { set_error("k must equal the number of template vertices (P:161)"); return SG2V_EINVAL; }
+    if (n_iter <= 0) { set_error("n_iter must be >= 1"); return SG2V_EINVAL; }
+    sg2v_options o;
+    if (op) o = *op; else if (g_opts_init) o = g_opts; else sg2v_options_default(&o);
+    if (o.precision < SG2V_F32 || o.precision > SG2V_U64) { set_error("bad precision"); return SG2V_EINVAL; }
+    if (o.mode != 0 || o.nccl_comm) { set_error("only mode 0 (replicas) is implemented"); return SG2V_EINVAL; }
+    if (o.iter_stride == 0) o.iter_stride = 1;
+    const int dev = g->device;
+    int prev_dev = 0;
+    cudaGetDevice(&prev_dev);
+    sg2v_status st = ensure_device(dev);
+    if (st != SG2V_OK) return st;
+    struct Restore { int d; ~Restore() { cudaSetDevice(d); } } restore{prev_dev};
+    const bool u64mode = o.precision == SG2V_U64;
+    std::vector<double> resf(n_iter, 0.0);
+    std::vector<uint64_t> resu(n_iter, 0);
+    cudaStream_t s = (cudaStream_t)o.stream;
+
+    if (k == 1 || g->n == 0) {
+        // single-vertex template: every vertex is a colourful embedding; empty graph: 0
+        for (int64_t q = 0; q < n_iter; ++q) { resf[q] = (double)g->n; resu[q] = (uint64_t)g->n; }
+        if (o.row_values && g->n > 0) {
+            std::vector<uint64_t> ones_u(g->n, 1);
+            std::vector<double> ones_f(g->n, 1.0);
+            const void *srcp = u64mode ? (const void *)ones_u.data() : (const void *)ones_f.data();
+            SG2V_CK(cudaMemcpy(o.row_values, srcp, g->n * 8, cudaMemcpyHostToDevice));
+        }
+    } else {
+        Plan *pl = nullptr;
+        st = get_plan(g->n, g->nnz, g->device, *t, o.precision, true, &pl);
+        if (st != SG2V_OK) return st;
+        char *ws = (char *)o.workspace;
+        bool own = false;
+        if (ws) {
+            if (o.workspace_bytes < (uint64_t)pl->ws_bytes) {
+                set_error("workspace too small: need " + std::to_string(pl->ws_bytes) + " bytes");
+                return SG2V_ENOMEM;
+            }
+        } else {
+            size_t fr = 0, tot = 0;
+            cudaMemGetInfo(&fr, &tot);
+            uint64_t budget = o.mem_budget_bytes ? o.mem_budget_bytes : (uint64_t)fr;
+            if ((uint64_t)pl->ws_bytes > budget) {
+                set_error("ENOMEM: plan needs " + std::to_string(pl->ws_bytes) + " bytes of device memory, budget " +
+                          std::to_string(budget));
+                return SG2V_ENOMEM;
+            }
+            SG2V_CK(cudaMalloc(&ws, pl->ws_bytes));
+            own = true;
+        }
+        struct Free { char *p; bool own; ~Free() { if (own) cudaFree(p); } } freer{ws, own};
+        if (o.mem_budget_bytes && (uint64_t)pl->ws_bytes > o.mem_budget_bytes) {
+            set_error("ENOMEM: plan needs " + std::to_string(pl->ws_bytes) + " bytes, budget " +
+                      std::to_string(o.mem_budget_bytes));
+            return SG2V_ENOMEM;
+        }
+        uint8_t *colors = (uint8_t *)(ws + pl->off_colors);
+        void *H = ws + pl->off_hist;
+        void *rowval = ws + pl->off_rowval;
+        void *partial = ws + pl->off_partial;
+        char *results = ws + pl->off_results;
+        std::vector<uint64_t> host_ring(kResultsRing);
+        int64_t base = 0;
+        for (int64_t q = 0; q < n_iter; ++q) {
+            const int64_t j = o.iter_offset + q * o.iter_stride;
+            int rc = launch_colorize(seed, j, g->n, k, colors, s);
+            if (rc) return cuda_fail("colorize", rc);
+            if (pl->need_hist && (rc = launch_hist(*g, *pl, colors, H, s))) return cuda_fail("hist", rc);
+            for (const Step &stp : pl->steps) {
+                rc = launch_step(*g, *pl, stp, colors, H, ws, rowval, s);
+                if (rc == -1) {
+                    set_error("row too wide for on-chip B (shared memory > 227 KB)");
+                    return SG2V_ENOMEM;
+                }
+                if (rc) return cuda_fail("step", rc);
+            }
+            rc = launch_reduce(*pl, g->n, rowval, partial, results + (q - base) * 8, s);
+            if (rc) return cuda_fail("reduce", rc);
+            if (q - base + 1 == kResultsRing || q == n_iter - 1) {
+                int64_t cnt = q - base + 1;
+                SG2V_CK(cudaMemcpyAsync(host_ring.data(), results, cnt * 8, cudaMemcpyDeviceToHost, s));
+                SG2V_CK(cudaStreamSynchronize(s));
+                for (int64_t r = 0; r < cnt; ++r) {
+                    if (u64mode) resu[base + r] = host_ring[r];
+                    else std::memcpy(&resf[base + r], &host_ring[r], 8);
+                }
+                base = q + 1;
+            }
+        }
+        if (o.row_values) {
+            SG2V_CK(cudaMemcpyAsync(o.row_values, rowval, g->n * 8, cudaMemcpyDeviceToDevice, s));
+            SG2V_CK(cudaStreamSynchronize(s));
+        }
+    }
+    bool finite = true;
+    double sum = 0.0;
+    for (int64_t q = 0; q < n_iter; ++q) {
+        if (colorful_out) colorful_out[q] = u64mode ? (double)resu[q] : resf[q];
+        if (colorful_u64_out) colorful_u64_out[q] = u64mode ? resu[q] : (uint64_t)resf[q];
+        if (!u64mode) {
+            if (!std::isfinite(resf[q])) finite = false;
+            sum += resf[q];
+        }
+    }
+    if (estimate_out)
+        *estimate_out = u64mode ? std::nan("") : sum / (double)n_iter / (t->P * t->alpha);
+    if (!finite) {
+        set_error("EOVERFLOW: a colourful count is not finite in F32 (use F64 or U64)");
+        return SG2V_EOVERFLOW;
+    }
+    return SG2V_OK;
+}
+
+sg2v_status sg2v_count(const sg2v_graph *g, const sg2v_template *t, int32_t k, int64_t n_iter, uint64_t seed,
+                       double *estimate_out, double *colorful_out, uint64_t *colorful_u64_out) {
+    return sg2v_count_ex(g, t, k, n_iter, seed, nullptr, estimate_out, colorful_out, colorful_u64_out);
+}
+
+sg2v_status sg2v_profile_enable(int32_t on) {
+    std::lock_guard<std::mutex> lk(g_prof_mu);
+    for (auto &r : g_prof) { g_ev_pool.push_back(r.a); g_ev_pool.push_back(r.b); }
+    g_prof.clear();
+    g_prof_on = on != 0;
+    return SG2V_OK;
+}
+
+sg2v_status sg2v_profile_read(int64_t launches[5], double ms[5], double bytes[5]) {
+    std::lock_guard<std::mutex> lk(g_prof_mu);
+    for (int c = 0; c < 5; ++c) { launches[c] = 0; ms[c] = 0.0; bytes[c] = 0.0; }
+    for (auto &r : g_prof) {
+        cudaError_t e = cudaEventSynchronize(r.b);
+        if (e != cudaSuccess) return cuda_fail("profile event", e);
+        float t = 0.f;
+        cudaEventElapsedTime(&t, r.a, r.b);
+        launches[r.cls] += 1;
+        ms[r.cls] += t;
+        bytes[r.cls] += r.bytes;
+    }
+    return SG2V_OK;
+}
+
+}  // extern "C"

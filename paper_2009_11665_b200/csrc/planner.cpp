@@ -1,0 +1,429 @@
+// planner.cpp — host planner of the colour-coding DP (layer P of SURVEY §1).
+//
+//  * template validation + α = |Aut(T)| (unrooted, AHU canonical forms)
+//  * partition search: root ρ and cut order chosen by a cost
+//    model of the B200 kernels (the count is invariant, SURVEY finding 1)
+//  * children-first schedule ordered to minimise the peak live set,
+//    with each table freed right after its parent's eMA
+//  * workspace layout (first-fit arena) and the colour-set index tables:
+//    column I_s of a colour set S is its COLEX rank among |S|-subsets of [k]
+//    (the paper leaves the map open; the oracle uses lexicographic on
+//    purpose so the two share nothing).
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <functional>
+#include <limits>
+#include <sstream>
+
+#include "sg2v_internal.h"
+
+namespace sg2v {
+
+int64_t binom(int n, int r) {
+    if (r < 0 || n < 0 || r > n) return 0;
+    static int64_t tab[33][33];
+    static bool init = false;
+    if (!init) {
+        for (int a = 0; a <= 32; ++a) {
+            tab[a][0] = 1;
+            for (int b = 1; b <= 32; ++b) tab[a][b] = (a == 0) ? 0 : tab[a - 1][b - 1] + tab[a - 1][b];
+        }
+        init = true;
+    }
+    return tab[n][r];
+}
+
+// colex rank of a subset mask among subsets of equal size: Σ_t C(e_t, t+1)
+static int64_t colex_rank(uint32_t mask) {
+    int64_t r = 0;
+    int t = 0;
+    while (mask) {
+        int e = __builtin_ctz(mask);
+        mask &= mask - 1;
+        r += binom(e, t + 1);
+        ++t;
+    }
+    return r;
+}
+
+// every s-subset of [k] in increasing mask order (= colex order), Gosper's hack
+static void for_each_subset(int k, int s, const std::function<void(uint32_t)> &f) {
+    if (s == 0) { f(0u); return; }
+    uint64_t m = (1ull << s) - 1, lim = 1ull << k;
+    while (m < lim) {
+        f((uint32_t)m);
+        uint64_t c = m & (~m + 1), r = m + c;
+        m = (((r ^ m) >> 2) / c) | r;
+    }
+}
+
+// ---------------------------------------------------------------------------
+sg2v_status validate_template(int k, const int32_t *edges, Template &t) {
+    if (k < 1 || k > 31) { set_error("k must be in [1, 31]"); return SG2V_EINVAL; }
+    if (k > 1 && !edges) { set_error("edges is NULL"); return SG2V_EINVAL; }
+    t.k = k;
+    t.adj.assign(k, {});
+    t.edges.clear();
+    for (int e = 0; e < k - 1; ++e) {
+        int u = edges[2 * e], v = edges[2 * e + 1];
+        if (u < 0 || v < 0 || u >= k || v >= k) { set_error("template vertex id out of [0,k)"); return SG2V_ENOTTREE; }
+        if (u == v) { set_error("template has a self-loop"); return SG2V_ENOTTREE; }
+        if (std::find(t.adj[u].begin(), t.adj[u].end(), v) != t.adj[u].end()) {
+            set_error("template has a duplicate edge");
+            return SG2V_ENOTTREE;
+        }
+        t.adj[u].push_back(v);
+        t.adj[v].push_back(u);
+        t.edges.push_back({u, v});
+    }
+    std::vector<int> seen(k, 0), stack{0};
+    seen[0] = 1;
+    int cnt = 1;
+    while (!stack.empty()) {
+        int v = stack.back();
+        stack.pop_back();
+        for (int w : t.adj[v])
+            if (!seen[w]) { seen[w] = 1; ++cnt; stack.push_back(w); }
+    }
+    if (cnt != k) { set_error("template is not connected (not a tree)"); return SG2V_ENOTTREE; }
+    for (auto &a : t.adj) std::sort(a.begin(), a.end());
+    return SG2V_OK;
+}
+
+// AHU: canonical string + automorphism count of the subtree at v (parent excluded)
+static std::pair<std::string, double> ahu(const Template &t, int v, int parent) {
+    std::vector<std::pair<std::string, double>> kids;
+    for (int c : t.adj[v])
+        if (c != parent) kids.push_back(ahu(t, c, v));
+    std::sort(kids.begin(), kids.end());
+    double aut = 1.0;
+    std::string canon = "(";
+    for (size_t i = 0; i < kids.size();) {
+        size_t j = i;
+        while (j < kids.size() && kids[j].first == kids[i].first) ++j;
+        for (size_t q = i; q < j; ++q) { aut *= kids[q].second; canon += kids[q].first; }
+        for (size_t m = 2; m <= j - i; ++m) aut *= (double)m;   // permute identical subtrees
+        i = j;
+    }
+    canon += ")";
+    return {canon, aut};
+}
+
+double automorphisms(const Template &t) {
+    int k = t.k;
+    if (k <= 2) return k == 1 ? 1.0 : 2.0;
+    std::vector<int> deg(k);
+    std::vector<int> layer;
+    for (int v = 0; v < k; ++v) {
+        deg[v] = (int)t.adj[v].size();
+        if (deg[v] == 1) layer.push_back(v);
+    }
+    int left = k;
+    while (left > 2) {                       // strip leaves to the centre
+        left -= (int)layer.size();
+        std::vector<int> nxt;
+        for (int v : layer)
+            for (int u : t.adj[v])
+                if (--deg[u] == 1) nxt.push_back(u);
+        layer = nxt;
+    }
+    if (layer.size() == 1) return ahu(t, layer[0], -1).second;
+    auto a = ahu(t, layer[0], layer[1]);
+    auto b = ahu(t, layer[1], layer[0]);
+    return a.second * b.second * (a.first == b.first ? 2.0 : 1.0);
+}
+
+// ---------------------------------------------------------------------------
+// Partition for a given root and child order.
+// ---------------------------------------------------------------------------
+struct Chain {
+    std::vector<Node> nodes;
+    int top = -1;
+};
+
+static Chain build_chain(const Template &t, int root, int policy) {
+    int k = t.k;
+    std::vector<std::vector<int>> children(k);
+    std::vector<int> sub(k, 1), parent(k, -1), order;
+    std::vector<int> st{root};
+    parent[root] = root;
+    while (!st.empty()) {
+        int v = st.back();
+        st.pop_back();
+        order.push_back(v);
+        for (int w : t.adj[v])
+            if (parent[w] < 0) { parent[w] = v; children[v].push_back(w); st.push_back(w); }
+    }
+    for (int i = (int)order.size() - 1; i >= 0; --i) {
+        int v = order[i];
+        for (int c : children[v]) sub[v] += sub[c];
+    }
+    for (int v = 0; v < k; ++v) {
+        auto &ch = children[v];
+        if (policy == 0)       // smallest subtree cut first (ties: lowest id)
+            std::sort(ch.begin(), ch.end(), [&](int a, int b) { return sub[a] != sub[b] ? sub[a] < sub[b] : a < b; });
+        else if (policy == 1)  // largest subtree cut first
+            std::sort(ch.begin(), ch.end(), [&](int a, int b) { return sub[a] != sub[b] ? sub[a] > sub[b] : a < b; });
+        else
+            std::sort(ch.begin(), ch.end());
+    }
+    Chain c;
+    std::function<int(int, int)> build = [&](int r, int j) -> int {
+        Node nd;
+        nd.r = r;
+        nd.j = j;
+        nd.size = 1;
+        for (size_t q = j; q < children[r].size(); ++q) nd.size += sub[children[r][q]];
+        if (j < (int)children[r].size()) {
+            nd.active = build(r, j + 1);                 // keeps ρ
+            nd.passive = build(children[r][j], 0);       // rooted at τ
+        }
+        c.nodes.push_back(nd);
+        return (int)c.nodes.size() - 1;
+    };
+    c.top = build(root, 0);
+    return c;
+}
+
+static int64_t round_up(int64_t x, int64_t m) { return (x + m - 1) / m * m; }
+
+static int pick_gt(int64_t cols, int vn) {
+    // threads per row group: enough lanes that R=4 vectors per lane cover the row
+    int64_t nvec = (cols + vn - 1) / vn;
+    int64_t want = (nvec + 3) / 4;
+    int gt = 4;
+    while (gt < want && gt < 256) gt *= 2;
+    return gt;
+}
+
+static constexpr double kHbm = 6.5e12;     // B/s, MEASURED_PEAKS hbm_gbs (planning only)
+static constexpr double kTermRate = 2.0e12; // eMA terms/s (smem-bound estimate)
+
+// Build steps, schedule, buffers and the model for one chain.
+static bool plan_chain(const Template &t, const Chain &c, int root, int64_t n, int64_t nnz,
+                       sg2v_precision prec, Plan &pl) {
+    const int k = t.k;
+    pl = Plan();
+    pl.k = k;
+    pl.root = root;
+    pl.prec = prec;
+    pl.elem = (prec == SG2V_F32) ? 4 : 8;
+    const int vn = 16 / pl.elem;
+    pl.nodes = c.nodes;
+    const double E = pl.elem;
+
+    // --- children-first order minimising the peak (Sethi–Ullman style) ---
+    std::vector<int64_t> out_bytes(pl.nodes.size(), 0);
+    for (size_t i = 0; i < pl.nodes.size(); ++i) {
+        const Node &nd = pl.nodes[i];
+        if (nd.active >= 0 && (int)i != c.top)
+            out_bytes[i] = n * round_up(binom(k, nd.size), vn) * pl.elem;
+    }
+    std::vector<int> sched;
+    std::function<int64_t(int, std::vector<int> &)> order = [&](int v, std::vector<int> &seq) -> int64_t {
+        const Node &nd = pl.nodes[v];
+        if (nd.active < 0) return 0;
+        std::vector<int> sa, sp;
+        int64_t pa = order(nd.active, sa), pp = order(nd.passive, sp);
+        int64_t oa = out_bytes[nd.active], op = out_bytes[nd.passive], os = out_bytes[v];
+        int64_t first_a = std::max({pa, oa + pp, oa + op + os});
+        int64_t first_p = std::max({pp, op + pa, oa + op + os});
+        if (first_a <= first_p) {
+            seq.insert(seq.end(), sa.begin(), sa.end());
+            seq.insert(seq.end(), sp.begin(), sp.end());
+        } else {
+            seq.insert(seq.end(), sp.begin(), sp.end());
+            seq.insert(seq.end(), sa.begin(), sa.end());
+        }
+        seq.push_back(v);
+        return std::min(first_a, first_p);
+    };
+    order(c.top, sched);
+
+    // --- first-fit arena over the schedule ---
+    std::vector<int> node_buf(pl.nodes.size(), -1);
+    std::vector<std::pair<int64_t, int64_t>> live;  // (offset, bytes) sorted by offset
+    int64_t arena = 0;
+    auto alloc = [&](int64_t bytes) -> int64_t {
+        int64_t pos = 0;
+        std::sort(live.begin(), live.end());
+        for (auto &iv : live) {
+            if (iv.first - pos >= bytes) break;
+            pos = std::max(pos, round_up(iv.first + iv.second, 256));
+        }
+        live.push_back({pos, bytes});
+        arena = std::max(arena, pos + bytes);
+        return pos;
+    };
+    auto release = [&](int b) {
+        if (b < 0) return;
+        for (size_t q = 0; q < live.size(); ++q)
+            if (live[q].first == pl.bufs[b].offset) { live.erase(live.begin() + q); break; }
+    };
+
+    double model = 0.0, alg_total = 0.0;
+    for (int v : sched) {
+        const Node &nd = pl.nodes[v];
+        Step st;
+        st.node = v;
+        st.s = nd.size;
+        st.a = pl.nodes[nd.active].size;
+        st.p = pl.nodes[nd.passive].size;
+        st.top = (v == c.top);
+        st.src = (st.p == 1) ? SRC_HIST : SRC_GATHER;
+        st.comb = (st.a == 1) ? COMB_ACTIVE_LEAF : COMB_GENERAL;
+        st.cs = st.top ? 1 : binom(k, st.s);
+        st.ca = binom(k, st.a);
+        st.cp = binom(k, st.p);
+        st.lds = st.top ? 1 : round_up(st.cs, vn);
+        st.lda = round_up(st.ca, vn);
+        st.ldp = (st.src == SRC_HIST) ? round_up(k, vn) : round_up(st.cp, vn);
+        st.buf_a = node_buf[nd.active];
+        st.buf_p = node_buf[nd.passive];
+        if (st.src == SRC_HIST) pl.need_hist = true;
+        if (!st.top) {
+            Buffer b;
+            b.bytes = n * st.lds * pl.elem;
+            b.offset = alloc(b.bytes);
+            pl.bufs.push_back(b);
+            st.buf_out = (int)pl.bufs.size() - 1;
+            node_buf[v] = st.buf_out;
+        }
+        release(st.buf_a);
+        release(st.buf_p);
+
+        // algorithmic bytes (useful columns only) and the model (sector-rounded)
+        double bytes = 0.0, mbytes = 0.0;
+        const bool top_leaf = st.top && st.comb == COMB_ACTIVE_LEAF;
+        if (top_leaf) {
+            if (st.src == SRC_GATHER) {
+                bytes = nnz * 4.0 + nnz * E + n * 9.0;
+                mbytes = nnz * 4.0 + nnz * 32.0 + n * 16.0;
+            } else {
+                bytes = mbytes = n * (E + 9.0);
+            }
+        } else {
+            double gather = (st.src == SRC_GATHER) ? nnz * 4.0 + nnz * (double)st.cp * E + n * 12.0
+                                                   : n * (double)k * E;
+            double mg = (st.src == SRC_GATHER) ? nnz * 4.0 + nnz * (double)round_up(st.cp * pl.elem, 32) + n * 12.0
+                                               : n * (double)st.ldp * E;
+            double ma = (st.comb == COMB_GENERAL) ? n * (double)st.ca * E : n * 1.0;
+            double w = st.top ? n * 8.0 : n * (double)st.cs * E;
+            bytes = gather + ma + w;
+            mbytes = mg + ma + w;
+        }
+        st.nterms = (st.comb == COMB_GENERAL) ? (st.top ? binom(k, st.a) : binom(st.s, st.a)) : 1;
+        st.ema_terms = (st.comb == COMB_GENERAL) ? (double)n * (double)st.cs * (double)st.nterms : 0.0;
+        st.alg_bytes = bytes;
+        st.gt = pick_gt(std::max({st.ldp, st.lds, st.comb == COMB_GENERAL ? st.lda : 0}), vn);
+        model += mbytes / kHbm + st.ema_terms / kTermRate;
+        alg_total += bytes;
+        pl.steps.push_back(st);
+    }
+    pl.tables_bytes = round_up(arena, 256);
+    pl.ldh = round_up(k, vn);
+    pl.hist_bytes = pl.need_hist ? n * pl.ldh * pl.elem : 0;
+    if (pl.need_hist) {
+        double hb = nnz * 4.0 + nnz * 1.0 + n * 12.0 + n * (double)k * E;
+        model += (nnz * 4.0 + nnz * 32.0 + pl.hist_bytes) / kHbm;
+        alg_total += hb;
+    }
+    pl.model_time = model;
+    pl.alg_bytes_total = alg_total;
+
+    // workspace layout
+    int64_t off = pl.tables_bytes;
+    pl.off_colors = off;  off = round_up(off + std::max<int64_t>(n, 1) + 16, 256);
+    pl.off_hist = off;    off = round_up(off + pl.hist_bytes, 256);
+    pl.off_rowval = off;  off = round_up(off + std::max<int64_t>(n, 1) * 8, 256);
+    pl.off_partial = off; off = round_up(off + kReduceBlocks * 8, 256);
+    pl.off_results = off; off = round_up(off + kResultsRing * 8, 256);
+    pl.ws_bytes = off;
+    return true;
+}
+
+static bool build_index(Plan &pl) {
+    const int k = pl.k;
+    const uint32_t full = (k == 32) ? 0xffffffffu : ((1u << k) - 1);
+    pl.index.clear();
+    for (Step &st : pl.steps) {
+        st.idx_off = (int64_t)pl.index.size();
+        if (st.top && st.comb == COMB_ACTIVE_LEAF) {
+            // colorful_i = B(i, [k] \ {c(i)}): column per colour x
+            for (int x = 0; x < k; ++x) pl.index.push_back((int32_t)colex_rank(full ^ (1u << x)));
+            pl.top_leaf_col_off = (int)st.idx_off;
+        } else if (st.comb == COMB_ACTIVE_LEAF) {
+            // M_s(i,S) = [c(i) ∈ S]·B(i, S \ {c(i)}): map[x][o]
+            double need = (double)k * (double)st.cs;
+            if (need > 1.5e9) { set_error("index table too large"); return false; }
+            std::vector<uint32_t> outs;
+            outs.reserve(st.cs);
+            for_each_subset(k, st.s, [&](uint32_t m) { outs.push_back(m); });
+            for (int x = 0; x < k; ++x)
+                for (uint32_t S : outs)
+                    pl.index.push_back((S >> x & 1u) ? (int32_t)colex_rank(S ^ (1u << x)) : -1);
+        } else {
+            // GENERAL: (I_a, I_p) for every split of every output colour set
+            double need = 2.0 * (double)st.cs * (double)st.nterms;
+            if (need > 1.5e9) { set_error("split table too large"); return false; }
+            auto emit = [&](uint32_t S) {
+                for (uint32_t sub = S;; sub = (sub - 1) & S) {
+                    if (__builtin_popcount(sub) == st.a) {
+                        pl.index.push_back((int32_t)colex_rank(sub));
+                        pl.index.push_back((int32_t)colex_rank(S ^ sub));
+                    }
+                    if (sub == 0) break;
+                }
+            };
+            if (st.top) emit(full);
+            else for_each_subset(k, st.s, emit);
+        }
+    }
+    if (pl.index.empty()) pl.index.push_back(0);
+    return true;
+}
+
+sg2v_status make_plan(const Template &t, int64_t n, int64_t nnz, sg2v_precision prec,
+                      std::unique_ptr<Plan> &out) {
+    std::unique_ptr<Plan> best;
+    int r0 = 0, r1 = t.k - 1;
+    if (t.root_hint >= 0) r0 = r1 = t.root_hint;
+    for (int root = r0; root <= r1; ++root) {
+        for (int policy = 0; policy < 3; ++policy) {
+            Chain c = build_chain(t, root, policy);
+            auto pl = std::make_unique<Plan>();
+            plan_chain(t, c, root, n, nnz, prec, *pl);
+            bool better = !best || pl->model_time < best->model_time * (1 - 1e-9) ||
+                          (pl->model_time <= best->model_time * (1 + 1e-9) && pl->ws_bytes < best->ws_bytes);
+            if (better) best = std::move(pl);
+        }
+    }
+    if (!build_index(*best)) return SG2V_ENOMEM;
+    out = std::move(best);
+    return SG2V_OK;
+}
+
+std::string Plan::describe() const {
+    std::ostringstream o;
+    o << "{\"k\":" << k << ",\"root\":" << root << ",\"elem\":" << elem
+      << ",\"precision\":\"" << (prec == SG2V_F32 ? "f32" : prec == SG2V_F64 ? "f64" : "u64") << "\""
+      << ",\"need_hist\":" << (need_hist ? "true" : "false") << ",\"hist_bytes\":" << hist_bytes
+      << ",\"tables_bytes\":" << tables_bytes << ",\"workspace_bytes\":" << ws_bytes
+      << ",\"model_seconds\":" << model_time << ",\"alg_bytes\":" << alg_bytes_total << ",\"steps\":[";
+    for (size_t i = 0; i < steps.size(); ++i) {
+        const Step &s = steps[i];
+        o << (i ? "," : "") << "{\"s\":" << s.s << ",\"a\":" << s.a << ",\"p\":" << s.p
+          << ",\"top\":" << (s.top ? "true" : "false")
+          << ",\"src\":\"" << (s.src == SRC_GATHER ? "gather" : "hist") << "\""
+          << ",\"comb\":\"" << (s.comb == COMB_ACTIVE_LEAF ? "active_leaf" : "general") << "\""
+          << ",\"cs\":" << s.cs << ",\"ca\":" << s.ca << ",\"cp\":" << s.cp
+          << ",\"lds\":" << s.lds << ",\"ldp\":" << s.ldp << ",\"nterms\":" << s.nterms
+          << ",\"gt\":" << s.gt << ",\"alg_bytes\":" << s.alg_bytes << ",\"ema_terms\":" << s.ema_terms << "}";
+    }
+    o << "]}";
+    return o.str();
+}
+
+}  // namespace sg2v

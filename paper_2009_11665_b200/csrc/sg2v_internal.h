@@ -1,0 +1,123 @@
+// sg2v_internal.h — host-side structures shared by the C ABI, the planner and
+// the kernel launchers of libsg2v.so.  Nothing here is visible through the ABI.
+#pragma once
+
+#include <cstddef>
+#include <cstdint>
+#include <map>
+#include <memory>
+#include <string>
+#include <tuple>
+#include <vector>
+
+#include "../../include/sg2v.h"
+
+namespace sg2v {
+
+void set_error(const std::string &msg);
+
+// ---------------------------------------------------------------------------
+// Graph: device CSR + degree-descending processing order.
+// ---------------------------------------------------------------------------
+struct Graph {
+    int64_t n = 0, nnz = 0;
+    int device = 0;
+    int64_t *d_rowptr = nullptr;
+    int32_t *d_col = nullptr;
+    int32_t *d_order = nullptr;  // rows sorted by degree, descending
+    int64_t max_deg = 0;
+};
+
+// ---------------------------------------------------------------------------
+// Plan of one colouring (P:162-170 partition, Alg. 5 schedule P:443-457).
+// ---------------------------------------------------------------------------
+enum StepSrc { SRC_GATHER = 0, SRC_HIST = 1 };        // B = A·M_p  |  B = H (leaf passive)
+enum StepComb { COMB_ACTIVE_LEAF = 0, COMB_GENERAL = 1 };
+
+struct Node {            // sub-template T_s: vertex r with children[r][j..] + subtrees
+    int r = 0, j = 0;
+    int size = 1;
+    int active = -1, passive = -1;  // node ids, -1 for a leaf
+};
+
+struct Step {
+    int node = 0;
+    int s = 0, a = 0, p = 0;
+    bool top = false;
+    StepSrc src = SRC_GATHER;
+    StepComb comb = COMB_ACTIVE_LEAF;
+    int64_t cs = 0, ca = 0, cp = 0;        // dense column counts C(k,·)
+    int64_t lds = 0, lda = 0, ldp = 0;     // padded row strides (elements)
+    int buf_out = -1, buf_a = -1, buf_p = -1;  // workspace buffers (-1: none / leaf / H)
+    int64_t idx_off = 0;                   // int32 offset into the plan's index blob
+    int64_t nterms = 0;                    // splits per output (GENERAL)
+    int gt = 32;                           // threads per row group (step kernel)
+    double alg_bytes = 0.0;                // algorithmic HBM bytes
+    double ema_terms = 0.0;
+};
+
+struct Buffer {
+    int64_t offset = 0, bytes = 0;
+};
+
+struct Plan {
+    int k = 0, root = 0;
+    int elem = 4;                 // sizeof element
+    sg2v_precision prec = SG2V_F32;
+    std::vector<Node> nodes;
+    std::vector<Step> steps;      // children-first order
+    bool need_hist = false;
+    int64_t ldh = 0;              // histogram row stride (elements)
+    std::vector<Buffer> bufs;     // count tables (offsets inside the workspace)
+    int64_t tables_bytes = 0;     // peak of the table arena
+    int64_t off_colors = 0, off_hist = 0, off_rowval = 0, off_partial = 0, off_results = 0;
+    int64_t ws_bytes = 0;
+    std::vector<int32_t> index;   // concatenated index tables (host copy)
+    int32_t *d_index = nullptr;   // device copy (owned by the template's cache)
+    int top_leaf_col_off = -1;    // idx offset of topcol[k] when the top step is leaf-active
+    double model_time = 0.0;
+    double alg_bytes_total = 0.0;
+    int64_t hist_bytes = 0;
+    std::string describe() const;
+};
+
+static constexpr int kResultsRing = 4096;
+static constexpr int kReduceBlocks = 512;
+
+// ---------------------------------------------------------------------------
+// Template: validated tree, α, P, cached plans per (precision, n, nnz, device).
+// ---------------------------------------------------------------------------
+struct Template {
+    int k = 0;
+    int root_hint = -1;
+    std::vector<std::pair<int, int>> edges;
+    std::vector<std::vector<int>> adj;
+    double alpha = 1.0;
+    double P = 1.0;
+    std::map<std::tuple<int, int64_t, int64_t, int>, std::unique_ptr<Plan>> plans;
+    ~Template();
+};
+
+// planner.cpp
+sg2v_status validate_template(int k, const int32_t *edges, Template &t);
+double automorphisms(const Template &t);
+sg2v_status make_plan(const Template &t, int64_t n, int64_t nnz, sg2v_precision prec,
+                      std::unique_ptr<Plan> &out);
+int64_t binom(int n, int r);
+
+// kernels.cu — launchers; all return cudaError_t as int (0 = success)
+struct Profiler;
+int launch_colorize(uint64_t seed, int64_t j, int64_t n, int k, uint8_t *out, void *stream);
+int launch_hist(const Graph &g, const Plan &pl, const uint8_t *colors, void *H, void *stream);
+int launch_step(const Graph &g, const Plan &pl, const Step &st, const uint8_t *colors,
+                const void *H, char *tables, void *rowval, void *stream);
+int launch_reduce(const Plan &pl, int64_t n, const void *rowval, void *partial, void *result,
+                  void *stream);
+int graph_build_order(Graph &g, void *stream);
+int graph_validate(const Graph &g, int *bad, void *stream);
+
+// profiling (api.cpp)
+void prof_begin(int cls, void *stream);
+void prof_end(int cls, double bytes, void *stream);
+
+}  // namespace sg2v

@@ -1,0 +1,305 @@
+"""Thin ctypes binding of libsg2v.so (include/sg2v.h) — argument marshalling only.
+
+Every step of the hot path runs in the library's sm_100a kernels; PyTorch is
+used only for device memory (the workspace), the current CUDA stream and
+process groups.  There is no CPU fallback: if libsg2v.so is missing or no
+B200 is visible, calls raise.
+
+Names follow the C ABI: graph_load_csr, template_build, count, colorize,
+workspace_bytes, plan_describe, profile_enable / profile_read.
+"""
+from __future__ import annotations
+
+import ctypes
+import json
+import os
+
+import numpy as np
+
+from .build import LIB
+
+OK, EINVAL, ENOTTREE, ENOMEM, ECUDA, ENCCL, EOVERFLOW = range(7)
+F32, F64, U64 = 0, 1, 2
+PRECISIONS = {"f32": F32, "f64": F64, "u64": U64}
+GRAPH_VALIDATE, GRAPH_DEVICE_PTRS = 1, 2
+_NAMES = {1: "EINVAL", 2: "ENOTTREE", 3: "ENOMEM", 4: "ECUDA", 5: "ENCCL", 6: "EOVERFLOW"}
+
+
+class Sg2vError(RuntimeError):
+    def __init__(self, code, msg):
+        super().__init__(f"{_NAMES.get(code, code)}: {msg}")
+        self.code = code
+
+
+class Options(ctypes.Structure):
+    _fields_ = [
+        ("precision", ctypes.c_int),
+        ("iter_offset", ctypes.c_int64),
+        ("iter_stride", ctypes.c_int64),
+        ("mode", ctypes.c_int32),
+        ("nccl_comm", ctypes.c_void_p),
+        ("device", ctypes.c_int32),
+        ("mem_budget_bytes", ctypes.c_uint64),
+        ("col_tile", ctypes.c_int32),
+        ("stream", ctypes.c_void_p),
+        ("workspace", ctypes.c_void_p),
+        ("workspace_bytes", ctypes.c_uint64),
+        ("row_values", ctypes.c_void_p),
+    ]
+
+
+_lib = None
+SYMBOLS = ["sg2v_graph_load_csr", "sg2v_graph_free", "sg2v_template_build", "sg2v_template_free",
+           "sg2v_template_info", "sg2v_options_default", "sg2v_set_options", "sg2v_workspace_bytes",
+           "sg2v_count", "sg2v_count_ex", "sg2v_colorize", "sg2v_plan_describe", "sg2v_plan_describe_n", "sg2v_profile_enable",
+           "sg2v_profile_read", "sg2v_last_error", "sg2v_version"]
+
+
+def lib():
+    """dlopen libsg2v.so (raises if it was not built — no fallback)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB):
+            raise RuntimeError(f"{LIB} missing: run __graft_entry__.build() (no CPU fallback exists)")
+        L = ctypes.CDLL(LIB)
+        vp, i64, i32, u64 = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32, ctypes.c_uint64
+        P = ctypes.POINTER
+        L.sg2v_graph_load_csr.argtypes = [i64, vp, vp, i64, ctypes.c_uint32, P(vp)]
+        L.sg2v_graph_free.argtypes = [vp]
+        L.sg2v_graph_free.restype = None
+        L.sg2v_template_build.argtypes = [i32, vp, i32, P(vp)]
+        L.sg2v_template_free.argtypes = [vp]
+        L.sg2v_template_free.restype = None
+        L.sg2v_template_info.argtypes = [vp, P(i32), P(ctypes.c_double), P(ctypes.c_double)]
+        L.sg2v_options_default.argtypes = [P(Options)]
+        L.sg2v_options_default.restype = None
+        L.sg2v_set_options.argtypes = [P(Options)]
+        L.sg2v_workspace_bytes.argtypes = [vp, vp, ctypes.c_int, P(u64)]
+        L.sg2v_count.argtypes = [vp, vp, i32, i64, u64, vp, vp, vp]
+        L.sg2v_count_ex.argtypes = [vp, vp, i32, i64, u64, P(Options), vp, vp, vp]
+        L.sg2v_colorize.argtypes = [u64, i64, i64, i32, vp, vp]
+        L.sg2v_plan_describe.argtypes = [vp, vp, ctypes.c_int, vp, u64, P(u64)]
+        L.sg2v_plan_describe_n.argtypes = [i64, i64, vp, ctypes.c_int, vp, u64, P(u64)]
+        L.sg2v_profile_enable.argtypes = [i32]
+        L.sg2v_profile_read.argtypes = [vp, vp, vp]
+        L.sg2v_last_error.restype = ctypes.c_char_p
+        L.sg2v_version.restype = ctypes.c_char_p
+        for name in ("sg2v_graph_load_csr", "sg2v_template_build", "sg2v_template_info", "sg2v_set_options",
+                     "sg2v_workspace_bytes", "sg2v_count", "sg2v_count_ex", "sg2v_colorize",
+                     "sg2v_plan_describe", "sg2v_plan_describe_n", "sg2v_profile_enable", "sg2v_profile_read"):
+            getattr(L, name).restype = ctypes.c_int
+        _lib = L
+    return _lib
+
+
+def _check(rc):
+    if rc != OK:
+        raise Sg2vError(rc, lib().sg2v_last_error().decode())
+
+
+def _torch():
+    import torch
+    return torch
+
+
+def _cur_stream():
+    torch = _torch()
+    return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+class Graph:
+    """Device CSR handle (sg2v_graph_load_csr)."""
+
+    def __init__(self, handle, n, nnz):
+        self._h = handle
+        self.n = n
+        self.nnz = nnz
+
+    @property
+    def handle(self):
+        return self._h
+
+    def free(self):
+        if self._h:
+            lib().sg2v_graph_free(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:
+            pass
+
+
+class Template:
+    """Validated tree template (sg2v_template_build)."""
+
+    def __init__(self, handle, k, edges):
+        self._h = handle
+        self.k = k
+        self.edges = edges
+
+    @property
+    def handle(self):
+        return self._h
+
+    def info(self):
+        k = ctypes.c_int32()
+        a = ctypes.c_double()
+        p = ctypes.c_double()
+        _check(lib().sg2v_template_info(self._h, ctypes.byref(k), ctypes.byref(a), ctypes.byref(p)))
+        return {"k": k.value, "alpha": a.value, "P": p.value}
+
+    def free(self):
+        if self._h:
+            lib().sg2v_template_free(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:
+            pass
+
+
+def _set_stream_option(stream):
+    o = Options()
+    lib().sg2v_options_default(ctypes.byref(o))
+    o.stream = stream if stream is not None else _cur_stream()
+    return o
+
+
+def graph_load_csr(n, row_offsets, col_indices, validate=False, stream=None) -> Graph:
+    """row_offsets/col_indices: numpy arrays (host) or CUDA torch tensors (device)."""
+    flags = GRAPH_VALIDATE if validate else 0
+    if hasattr(row_offsets, "is_cuda") and row_offsets.is_cuda:
+        torch = _torch()
+        ro = row_offsets.to(torch.int64).contiguous()
+        ci = col_indices.to(torch.int32).contiguous()
+        flags |= GRAPH_DEVICE_PTRS
+        p_ro, p_ci, nnz = ro.data_ptr(), ci.data_ptr() if ci.numel() else None, ci.numel()
+        keep = (ro, ci)
+    else:
+        ro = np.ascontiguousarray(row_offsets, dtype=np.int64)
+        ci = np.ascontiguousarray(col_indices, dtype=np.int32)
+        p_ro = ro.ctypes.data
+        p_ci = ci.ctypes.data if ci.size else None
+        nnz = ci.size
+        keep = (ro, ci)
+    o = _set_stream_option(stream)
+    _check(lib().sg2v_set_options(ctypes.byref(o)))
+    h = ctypes.c_void_p()
+    _check(lib().sg2v_graph_load_csr(int(n), p_ro, p_ci, int(nnz), flags, ctypes.byref(h)))
+    del keep
+    return Graph(h, int(n), int(nnz))
+
+
+def template_build(k, edges, root_hint=-1) -> Template:
+    e = np.ascontiguousarray(np.asarray(edges, dtype=np.int32).reshape(-1)) if len(edges) else None
+    h = ctypes.c_void_p()
+    _check(lib().sg2v_template_build(int(k), e.ctypes.data if e is not None else None, int(root_hint),
+                                     ctypes.byref(h)))
+    return Template(h, int(k), list(edges))
+
+
+def workspace_bytes(graph: Graph, tmpl: Template, precision="f32") -> int:
+    b = ctypes.c_uint64()
+    _check(lib().sg2v_workspace_bytes(graph.handle, tmpl.handle, PRECISIONS[precision], ctypes.byref(b)))
+    return int(b.value)
+
+
+def plan_describe(graph: Graph, tmpl: Template, precision="f32") -> dict:
+    need = ctypes.c_uint64()
+    _check(lib().sg2v_plan_describe(graph.handle, tmpl.handle, PRECISIONS[precision], None, 0, ctypes.byref(need)))
+    buf = ctypes.create_string_buffer(int(need.value))
+    _check(lib().sg2v_plan_describe(graph.handle, tmpl.handle, PRECISIONS[precision], buf, need.value,
+                                    ctypes.byref(need)))
+    return json.loads(buf.value.decode())
+
+
+def plan_describe_n(n: int, nnz: int, tmpl: Template, precision="f32") -> dict:
+    """Host-only planning (no graph handle, no GPU)."""
+    need = ctypes.c_uint64()
+    _check(lib().sg2v_plan_describe_n(int(n), int(nnz), tmpl.handle, PRECISIONS[precision], None, 0,
+                                      ctypes.byref(need)))
+    buf = ctypes.create_string_buffer(int(need.value))
+    _check(lib().sg2v_plan_describe_n(int(n), int(nnz), tmpl.handle, PRECISIONS[precision], buf, need.value,
+                                      ctypes.byref(need)))
+    return json.loads(buf.value.decode())
+
+
+class Workspace:
+    """Device workspace allocated by torch and lent to the library."""
+
+    def __init__(self, nbytes, device=None):
+        torch = _torch()
+        self.tensor = torch.empty(max(int(nbytes), 1), dtype=torch.uint8,
+                                  device=device if device is not None else "cuda")
+        self.nbytes = int(nbytes)
+
+    @property
+    def ptr(self):
+        return self.tensor.data_ptr()
+
+
+def count(graph: Graph, tmpl: Template, n_iter: int, seed: int, precision="f32", iter_offset=0,
+          iter_stride=1, workspace: Workspace | None = None, stream=None, row_values=None,
+          allow_overflow=False, mem_budget_bytes=0):
+    """sg2v_count_ex.  Returns (estimate, colorful) — colorful is float64[n_iter]
+    (F32/F64) or uint64[n_iter] (U64, residues mod 2^64).  row_values: optional
+    CUDA tensor (float64 or int64/uint64, n entries) receiving the per-vertex
+    values of the last colouring."""
+    prec = PRECISIONS[precision]
+    o = Options()
+    lib().sg2v_options_default(ctypes.byref(o))
+    o.precision = prec
+    o.iter_offset = int(iter_offset)
+    o.iter_stride = int(iter_stride)
+    o.stream = stream if stream is not None else _cur_stream()
+    o.mem_budget_bytes = int(mem_budget_bytes)
+    if workspace is None and graph.n > 0 and tmpl.k > 1:
+        workspace = Workspace(workspace_bytes(graph, tmpl, precision))
+    if workspace is not None:
+        o.workspace = workspace.ptr
+        o.workspace_bytes = workspace.nbytes
+    if row_values is not None:
+        o.row_values = row_values.data_ptr()
+    est = ctypes.c_double()
+    if prec == U64:
+        out = np.zeros(n_iter, dtype=np.uint64)
+        rc = lib().sg2v_count_ex(graph.handle, tmpl.handle, tmpl.k, int(n_iter), int(seed) & (2**64 - 1),
+                                 ctypes.byref(o), ctypes.byref(est), None, out.ctypes.data)
+    else:
+        out = np.zeros(n_iter, dtype=np.float64)
+        rc = lib().sg2v_count_ex(graph.handle, tmpl.handle, tmpl.k, int(n_iter), int(seed) & (2**64 - 1),
+                                 ctypes.byref(o), ctypes.byref(est), out.ctypes.data, None)
+    if rc == EOVERFLOW and allow_overflow:
+        return est.value, out
+    _check(rc)
+    return est.value, out
+
+
+def colorize(seed, j, n, k, out, stream=None):
+    """K-COLOR into a CUDA uint8 tensor `out` (n entries)."""
+    s = stream if stream is not None else _cur_stream()
+    _check(lib().sg2v_colorize(int(seed) & (2**64 - 1), int(j), int(n), int(k), out.data_ptr(), s))
+
+
+def profile_enable(on=True):
+    _check(lib().sg2v_profile_enable(1 if on else 0))
+
+
+KERNEL_CLASSES = ["color", "hist", "step", "top", "reduce"]
+
+
+def profile_read():
+    launches = np.zeros(5, np.int64)
+    ms = np.zeros(5, np.float64)
+    by = np.zeros(5, np.float64)
+    _check(lib().sg2v_profile_read(launches.ctypes.data, ms.ctypes.data, by.ctypes.data))
+    return {c: {"launches": int(launches[i]), "ms": float(ms[i]), "bytes": float(by[i])}
+            for i, c in enumerate(KERNEL_CLASSES)}
+
+
+def version() -> str:
+    return lib().sg2v_version().decode()

@@ -10,8 +10,8 @@ duplicates removed, self-loops dropped, column ids sorted inside each row.
 * small closed-form graphs (cycle, path, complete, "house+tail") used by the
   oracle pins (SURVEY §8(c) "What pins each part").
 
-Everything is numpy with ``default_rng(seed)``; the random stream is fixed by
-(seed, chunking) so the same arrays come out on every machine.
+ER uses numpy ``default_rng(seed)``; RMAT uses counter-hash uniforms in gen.c
+(thread-count independent), so the same arrays come out on every machine.
 """
 from __future__ import annotations
 
@@ -88,40 +88,48 @@ def erdos_renyi(n: int, m: int, seed: int = 1) -> CSR:
     return csr_from_edges(n, lo, hi, name=f"ER(n={n},m={m},seed={seed})")
 
 
+_GEN = None
+
+
+def _gen_lib():
+    """gcc-built helper (gen.c): RMAT draw + symmetrise/dedupe in C (numpy is too slow at 2e8)."""
+    global _GEN
+    if _GEN is None:
+        import ctypes
+        import os
+        import subprocess
+        here = os.path.dirname(os.path.abspath(__file__))
+        src, lib = os.path.join(here, "gen.c"), os.path.join(here, "libgen.so")
+        if not os.path.exists(lib) or os.path.getmtime(lib) < os.path.getmtime(src):
+            subprocess.check_call(["gcc", "-O2", "-fopenmp", "-fPIC", "-shared", "-o", lib, src])
+        L = ctypes.CDLL(lib)
+        L.gen_rmat.restype = ctypes.c_int64
+        L.gen_rmat.argtypes = [ctypes.c_int32, ctypes.c_int64, ctypes.c_double, ctypes.c_double,
+                               ctypes.c_double, ctypes.c_uint64, ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p]
+        _GEN = L
+    return _GEN
+
+
 def rmat(scale: int, m: int, a: float, b: float, c: float, seed: int = 1,
-         perm_seed: int | None = 7, chunk: int = 1 << 24) -> CSR:
+         perm_seed: int | None = 7) -> CSR:
     """RMAT(a,b,c,d=1-a-b-c) with m drawn directed edges over n = 2^scale vertices.
 
-    Each edge picks one quadrant per level (row bit set for quadrants c,d; column
-    bit set for b,d).  Vertex ids are then relabelled by a random permutation
-    (``perm_seed``) so degree is uncorrelated with id, then the edge set is
-    symmetrised and deduplicated (SURVEY §8(d) D4 recipe).
+    Each draw picks one quadrant per level (row bit set for quadrants c,d;
+    column bit for b,d) from a counter-hash uniform of (seed, edge, level);
+    vertex ids are relabelled by a random permutation (``perm_seed``) so degree
+    is uncorrelated with id; the edge set is symmetrised, self-loops dropped
+    and duplicates removed (SURVEY §8(d) D4 recipe).  Implemented in gen.c.
     """
     n = 1 << scale
-    rng = np.random.default_rng(seed)
-    us, vs = [], []
-    ab, abc = a + b, a + b + c
-    left = m
-    while left > 0:
-        cnt = min(chunk, left)
-        left -= cnt
-        u = np.zeros(cnt, dtype=np.int64)
-        v = np.zeros(cnt, dtype=np.int64)
-        for lvl in range(scale):
-            r = rng.random(cnt, dtype=np.float64)
-            bit = np.int64(1) << np.int64(scale - 1 - lvl)
-            row_bit = r >= ab
-            col_bit = ((r >= a) & (r < ab)) | (r >= abc)
-            u |= np.where(row_bit, bit, 0)
-            v |= np.where(col_bit, bit, 0)
-        us.append(u)
-        vs.append(v)
-    u = np.concatenate(us)
-    v = np.concatenate(vs)
-    if perm_seed is not None:
-        perm = np.random.default_rng(perm_seed).permutation(n).astype(np.int64)
-        u, v = perm[u], perm[v]
-    return csr_from_edges(n, u, v, name=f"RMAT(scale={scale},m={m},a={a},b={b},c={c},seed={seed})")
+    ro = np.zeros(n + 1, dtype=np.int64)
+    col = np.empty(max(2 * m, 1), dtype=np.int32)
+    nnz = _gen_lib().gen_rmat(scale, m, a, b, c, seed, -1 if perm_seed is None else perm_seed,
+                              ro.ctypes.data, col.ctypes.data)
+    if nnz < 0:
+        raise MemoryError("gen_rmat failed")
+    col = col[:nnz].copy()
+    return CSR(n=n, row_offsets=ro, col_indices=col,
+               name=f"RMAT(scale={scale},m={m},a={a},b={b},c={c},seed={seed})")
 
 
 def rmat_1m_like(scale: int = 20, edge_factor: float = 100.0, seed: int = 1) -> CSR:

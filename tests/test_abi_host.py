@@ -1,0 +1,109 @@
+"""Host-side checks of libsg2v.so (no GPU needed, runs with -m "not gpu").
+
+* the library loads and exports every symbol include/sg2v.h declares;
+* template validation (ENOTTREE / EINVAL);
+* α and P agree with the oracle's independent implementations;
+* the planner's schedules satisfy the partition invariants and its
+  table widths / traversal counts are the paper's;
+* without a GPU every device entry point fails loudly (no CPU fallback).
+"""
+import math
+import os
+import re
+
+import pytest
+
+import paper_2009_11665_b200 as sg
+from paper_2009_11665_b200.build import build as build_lib
+from sg2v_inputs import TEMPLATES, path_template, random_tree, star_template
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _built():
+    build_lib()
+
+
+def test_exports_every_declared_symbol():
+    hdr = open(os.path.join(ROOT, "include", "sg2v.h")).read()
+    declared = set(re.findall(r"\b(sg2v_[a-z0-9_]+)\s*\(", hdr))
+    assert declared, "no declarations parsed"
+    L = sg.lib()
+    for name in declared:
+        assert hasattr(L, name), f"{name} declared in sg2v.h but not exported"
+    assert declared == set(sg.sg2v.SYMBOLS)
+    assert "sm_100a" in sg.version()
+
+
+def test_template_validation():
+    with pytest.raises(sg.Sg2vError) as e:
+        sg.template_build(3, [(0, 1), (0, 1)])
+    assert e.value.code == 2
+    with pytest.raises(sg.Sg2vError) as e:
+        sg.template_build(4, [(0, 1), (1, 2), (0, 2)])  # cycle + isolated vertex
+    assert e.value.code == 2
+    with pytest.raises(sg.Sg2vError) as e:
+        sg.template_build(3, [(0, 1), (1, 3)])
+    assert e.value.code == 2
+    with pytest.raises(sg.Sg2vError) as e:
+        sg.template_build(0, [])
+    assert e.value.code == 1
+    with pytest.raises(sg.Sg2vError) as e:
+        sg.template_build(32, path_template(32))
+    assert e.value.code == 1
+    with pytest.raises(sg.Sg2vError) as e:
+        sg.template_build(3, path_template(3), root_hint=3)
+    assert e.value.code == 1
+
+
+def test_alpha_and_P_match_oracle(oracle):
+    cases = [(k, e) for k in range(1, 9) for e in (path_template(k), star_template(k), random_tree(k, 7 * k))]
+    cases += [(1 + max(max(x) for x in e), e) for n, e in TEMPLATES.items() if e]
+    for k, e in cases:
+        info = sg.template_build(k, e).info()
+        assert info["alpha"] == float(oracle.alpha(k, e)), (k, e)
+        assert math.isclose(info["P"], float(oracle.colorful_probability(k)), rel_tol=1e-15)
+
+
+@pytest.mark.parametrize("name", ["u3-1", "u5-2", "u7-2", "u10-2", "u12-1", "u15-1", "u17", "star9", "path9"])
+def test_plan_invariants(name):
+    e = TEMPLATES[name]
+    k = 1 + max(max(x) for x in e)
+    T = sg.template_build(k, e)
+    for prec in ("f32", "f64", "u64"):
+        d = sg.plan_describe_n(1 << 20, 200 << 20, T, prec)
+        steps = d["steps"]
+        assert len(steps) == k - 1                      # k-1 splits (2k-1 nodes)
+        assert steps[-1]["top"] and steps[-1]["s"] == k
+        elem = 4 if prec == "f32" else 8
+        for s in steps:
+            assert s["s"] == s["a"] + s["p"]
+            assert s["cp"] == math.comb(k, s["p"])         # C(k,|T_p|) traversals
+            assert s["ca"] == math.comb(k, s["a"])
+            if not s["top"]:
+                assert s["cs"] == math.comb(k, s["s"])
+                assert s["lds"] * elem % 16 == 0
+            if s["comb"] == "general":
+                assert s["nterms"] == (math.comb(k, s["a"]) if s["top"] else math.comb(s["s"], s["a"]))
+        assert d["workspace_bytes"] >= d["tables_bytes"] > 0 or k <= 2
+
+
+def test_root_hint_changes_plan_not_sizes():
+    k = 9
+    e = path_template(9)
+    d0 = sg.plan_describe_n(1000, 8000, sg.template_build(k, e, root_hint=0), "u64")
+    d4 = sg.plan_describe_n(1000, 8000, sg.template_build(k, e, root_hint=4), "u64")
+    assert d0["root"] == 0 and d4["root"] == 4
+    assert d0["steps"][-1]["a"] == 1                    # rooted at an end: leaf-active top
+    assert d4["steps"][-1]["a"] > 1
+
+
+def test_no_cpu_fallback():
+    import numpy as np
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    with pytest.raises(sg.Sg2vError) as e:
+        sg.graph_load_csr(3, np.array([0, 1, 2, 2]), np.array([1, 0], np.int32), stream=0)
+    assert e.value.code == 4

@@ -1,0 +1,240 @@
+"""GPU parity: the CUDA path (through the C ABI) vs the CPU oracle.
+
+Bars (BASELINE.json north_star):
+  * U64: bit-exact residues mod 2^64, every colouring, every config;
+  * F64: bit-exact while the oracle's max intermediate < 2^53, else rel 1e-12;
+  * F32: rel 1e-4 (bit-exact when the oracle's max intermediate < 2^24).
+Per-vertex values Σ_C M_0(i,·) are compared element by element.
+"""
+import math
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+import paper_2009_11665_b200 as sg  # noqa: E402
+from sg2v_inputs import (TEMPLATES, complete_graph, csr_from_edges, erdos_renyi,  # noqa: E402
+                         path_template, random_tree, rmat, star_template)
+
+
+def _k(e):
+    return 1 + max((max(x) for x in e), default=0)
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _dev():
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    torch.cuda.set_device(0)
+
+
+def _load(g):
+    return sg.graph_load_csr(g.n, g.row_offsets, g.col_indices, validate=True)
+
+
+def _rows(G, T, seed, j, prec):
+    dt = torch.int64 if prec == "u64" else torch.float64
+    rv = torch.zeros(max(G.n, 1), dtype=dt, device="cuda")
+    _, tot = sg.count(G, T, n_iter=1, seed=seed, iter_offset=j, precision=prec, row_values=rv,
+                      allow_overflow=True)
+    r = rv.cpu().numpy()[:G.n]
+    return tot[0], (r.view(np.uint64) if prec == "u64" else r)
+
+
+def _check_all(oracle, g, e, seeds_js, roots=(-1,), precs=("u64", "f64", "f32"), rows=True):
+    k = _k(e)
+    G = _load(g)
+    for root in roots:
+        T = sg.template_build(k, e, root_hint=root)
+        for seed, j in seeds_js:
+            cols = oracle.colors(seed, j, g.n, k)
+            want_u, want_ru = oracle.count(g, k, e, cols, rows=True)
+            want_f, vmax, want_rf = oracle.count(g, k, e, cols, arith=oracle.ARITH_F64, rows=True)
+            for prec in precs:
+                if rows:
+                    tot, r = _rows(G, T, seed, j, prec)
+                else:
+                    _, t = sg.count(G, T, n_iter=1, seed=seed, iter_offset=j, precision=prec, allow_overflow=True)
+                    tot, r = t[0], None
+                if prec == "u64":
+                    assert int(tot) == want_u, (root, seed, j)
+                    if r is not None:
+                        assert np.array_equal(r, want_ru)
+                elif prec == "f64":
+                    if vmax < 2 ** 53:
+                        assert tot == want_f
+                        if r is not None:
+                            assert np.array_equal(r, want_rf)
+                    else:
+                        assert math.isclose(tot, want_f, rel_tol=1e-12)
+                        if r is not None:
+                            assert np.allclose(r, want_rf, rtol=1e-12, atol=0)
+                else:
+                    if vmax < 2 ** 24:
+                        assert tot == want_f
+                        if r is not None:
+                            assert np.array_equal(r, want_rf)
+                    elif math.isfinite(tot):
+                        assert math.isclose(tot, want_f, rel_tol=1e-4)
+                        if r is not None:
+                            assert np.allclose(r, want_rf, rtol=1e-4, atol=1e-4 * max(1.0, float(want_rf.max())))
+
+
+# --------------------------------------------------------------------------- a1
+def test_colorize_matches_oracle(oracle):
+    n = 100_003
+    out = torch.empty(n, dtype=torch.uint8, device="cuda")
+    for seed, j, k in ((1, 0, 3), (42, 7, 17), (2**63 + 5, 123456, 31), (9, 2, 1)):
+        sg.colorize(seed, j, n, k, out)
+        assert np.array_equal(out.cpu().numpy(), oracle.colors(seed, j, n, k))
+
+
+# --------------------------------------------------------------------------- D1 (configs[0])
+def test_d1_u3_er1000_100_colourings(oracle):
+    g = erdos_renyi(1000, 4000, seed=1)
+    e = TEMPLATES["u3-1"]
+    G = _load(g)
+    T = sg.template_build(3, e)
+    want = [oracle.count(g, 3, e, oracle.colors(1, j, g.n, 3)) for j in range(100)]
+    for prec in ("u64", "f64", "f32"):
+        est, got = sg.count(G, T, n_iter=100, seed=1, precision=prec)
+        assert [int(x) for x in got] == want  # all values < 2^24: bit-exact in every mode
+        if prec != "u64":
+            P = math.factorial(3) / 27
+            assert math.isclose(est, sum(want) / 100 / (P * 2), rel_tol=1e-12)
+        else:
+            assert math.isnan(est)
+
+
+# --------------------------------------------------------------------------- template zoo
+ZOO = ["u2", "u3-1", "star4", "path4", "u5-2", "star5", "path6", "star6", "u7-2", "u10-2"]
+
+
+@pytest.mark.parametrize("name", ZOO)
+def test_zoo_small_rmat(oracle, name):
+    g = rmat(11, 30_000, 0.45, 0.22, 0.22, seed=3)
+    e = TEMPLATES[name]
+    roots = (-1, 0, _k(e) - 1)
+    _check_all(oracle, g, e, [(1, 0), (7, 3)], roots=roots)
+
+
+@pytest.mark.parametrize("k", [4, 6, 8, 9])
+def test_random_trees_all_roots(oracle, k):
+    g = erdos_renyi(300, 1500, seed=k)
+    e = random_tree(k, 31 * k)
+    _check_all(oracle, g, e, [(5, 1)], roots=tuple(range(-1, k)), precs=("u64",))
+
+
+def test_wide_rows_multiple_passes(oracle):
+    # u15-1: c_p up to C(15,7)=6435 -> several 1024-vector passes per row (fp32) and
+    # odd widths (ragged tails of the 16-B vectors); also u12-1
+    g = erdos_renyi(1500, 9000, seed=4)
+    _check_all(oracle, g, TEMPLATES["u15-1"], [(1, 0)], precs=("u64", "f64", "f32"))
+    _check_all(oracle, g, TEMPLATES["u12-1"], [(2, 5)], roots=(-1, 0, 5))
+
+
+def test_heavy_hub_and_isolated(oracle):
+    # one hub adjacent to every vertex + a sparse remainder + isolated vertices
+    n = 3000
+    rng = np.random.default_rng(0)
+    u = np.concatenate([np.zeros(n - 100, np.int64), rng.integers(1, n, 4000)])
+    v = np.concatenate([np.arange(1, n - 99), rng.integers(1, n, 4000)])
+    g = csr_from_edges(n + 50, u, v)
+    for name in ("u5-2", "path6", "star5"):
+        _check_all(oracle, g, TEMPLATES[name], [(3, 2)])
+
+
+# --------------------------------------------------------------------------- edge cases
+def test_k1_k2_and_tiny(oracle):
+    g = erdos_renyi(50, 200, seed=2)
+    G = _load(g)
+    T1 = sg.template_build(1, [])
+    _, c = sg.count(G, T1, n_iter=3, seed=1, precision="u64")
+    assert [int(x) for x in c] == [50] * 3
+    T2 = sg.template_build(2, [(0, 1)])
+    for j in range(3):
+        cols = oracle.colors(1, j, g.n, 2)
+        ed = g.edges()
+        want = 2 * int(np.sum(cols[ed[:, 0]] != cols[ed[:, 1]]))
+        _, c = sg.count(G, T2, n_iter=1, seed=1, iter_offset=j, precision="u64")
+        assert int(c[0]) == want
+    # n < k: no colourful embedding possible
+    gk = complete_graph(3)
+    _, c = sg.count(_load(gk), sg.template_build(5, TEMPLATES["u5-2"]), n_iter=2, seed=1, precision="u64")
+    assert list(c) == [0, 0]
+    # graph without edges
+    ge = csr_from_edges(10, [], [])
+    _, c = sg.count(_load(ge), sg.template_build(3, path_template(3)), n_iter=1, seed=1, precision="f32")
+    assert list(c) == [0.0]
+
+
+def test_empty_graph():
+    G = sg.graph_load_csr(0, np.zeros(1, np.int64), np.zeros(0, np.int32))
+    _, c = sg.count(G, sg.template_build(3, path_template(3)), n_iter=2, seed=1, precision="u64")
+    assert list(c) == [0, 0]
+
+
+def test_errors():
+    g = erdos_renyi(20, 40, seed=1)
+    G = _load(g)
+    T = sg.template_build(3, path_template(3))
+    with pytest.raises(sg.Sg2vError) as e:
+        sg.count(G, T, n_iter=0, seed=1)
+    assert e.value.code == sg.sg2v.EINVAL
+    # unsorted / asymmetric / self-loop CSR rejected by VALIDATE
+    bad = [
+        (np.array([0, 2, 3, 4]), np.array([2, 1, 0, 0], np.int32)),  # row 0 unsorted
+        (np.array([0, 1, 1, 1]), np.array([1], np.int32)),           # asymmetric
+        (np.array([0, 1, 1, 1]), np.array([0], np.int32)),           # self-loop
+    ]
+    for ro, ci in bad:
+        with pytest.raises(sg.Sg2vError) as e:
+            sg.graph_load_csr(3, ro, ci, validate=True)
+        assert e.value.code == sg.sg2v.EINVAL
+    # memory budget / workspace too small: ENOMEM before allocating
+    big = sg.template_build(12, path_template(12))
+    with pytest.raises(sg.Sg2vError) as e:
+        sg.count(G, big, n_iter=1, seed=1, workspace=sg.Workspace(16))
+    assert e.value.code == sg.sg2v.ENOMEM
+    o = sg.Options()
+    sg.lib().sg2v_options_default(o)
+    o.precision = sg.U64
+    o.mem_budget_bytes = 1024
+    rc = sg.lib().sg2v_count_ex(G.handle, big.handle, 12, 1, 1, o, None, None, None)
+    assert rc == sg.sg2v.ENOMEM and b"needs" in sg.lib().sg2v_last_error()
+
+
+def test_determinism_and_sharding():
+    g = rmat(12, 60_000, 0.45, 0.22, 0.22, seed=5)
+    G = _load(g)
+    T = sg.template_build(7, TEMPLATES["u7-2"])
+    _, a = sg.count(G, T, n_iter=8, seed=11, precision="f32")
+    _, b = sg.count(G, T, n_iter=8, seed=11, precision="f32")
+    assert np.array_equal(a, b)                                   # run-to-run bitwise
+    _, s0 = sg.count(G, T, n_iter=4, seed=11, iter_offset=0, iter_stride=2, precision="f32")
+    _, s1 = sg.count(G, T, n_iter=4, seed=11, iter_offset=1, iter_stride=2, precision="f32")
+    assert np.array_equal(a[0::2], s0) and np.array_equal(a[1::2], s1)  # replica shards
+
+
+def test_closed_form_tree_on_complete_graph(oracle):
+    # colorful = k!·Π_c n_c for any tree on K_n (SURVEY §8(c) pin 2), independent of the oracle
+    g = complete_graph(120)
+    G = _load(g)
+    for k, e in ((5, TEMPLATES["u5-2"]), (7, TEMPLATES["u7-2"]), (9, star_template(9))):
+        T = sg.template_build(k, e)
+        _, got = sg.count(G, T, n_iter=3, seed=4, precision="u64")
+        for j in range(3):
+            nc = np.bincount(oracle.colors(4, j, g.n, k), minlength=k)
+            want = math.factorial(k) * math.prod(int(x) for x in nc)
+            assert int(got[j]) == want % (1 << 64)
+
+
+def test_f32_close_to_f64_on_dense_graph():
+    g = complete_graph(200)
+    G = _load(g)
+    T = sg.template_build(8, path_template(8))
+    _, f = sg.count(G, T, n_iter=1, seed=1, precision="f32")
+    _, d = sg.count(G, T, n_iter=1, seed=1, precision="f64")
+    assert math.isclose(f[0], d[0], rel_tol=1e-4)
