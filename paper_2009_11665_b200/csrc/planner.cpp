@@ -349,6 +349,7 @@ static bool build_index(Plan &pl) {
     const uint32_t full = (k == 32) ? 0xffffffffu : ((1u << k) - 1);
     pl.index.clear();
     for (Step &st : pl.steps) {
+        while (pl.index.size() % 4) pl.index.push_back(0);   // 16-B aligned tables (int2 loads)
         st.idx_off = (int64_t)pl.index.size();
         if (st.top && st.comb == COMB_ACTIVE_LEAF) {
             // colorful_i = B(i, [k] \ {c(i)}): column per colour x

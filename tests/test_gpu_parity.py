@@ -50,9 +50,12 @@ def _check_all(oracle, g, e, seeds_js, roots=(-1,), precs=("u64", "f64", "f32"),
         T = sg.template_build(k, e, root_hint=root)
         for seed, j in seeds_js:
             cols = oracle.colors(seed, j, g.n, k)
-            want_u, want_ru = oracle.count(g, k, e, cols, rows=True)
-            want_f, vmax, want_rf = oracle.count(g, k, e, cols, arith=oracle.ARITH_F64, rows=True)
             for prec in precs:
+                # per-vertex values count embeddings with the ROOT mapped to i, so the
+                # oracle is rooted where the planner rooted (the total is root-free)
+                rho = sg.plan_describe(G, T, prec).get("root", 0) if k > 1 else 0
+                want_u, want_ru = oracle.count(g, k, e, cols, root=rho, rows=True)
+                want_f, vmax, want_rf = oracle.count(g, k, e, cols, root=rho, arith=oracle.ARITH_F64, rows=True)
                 if rows:
                     tot, r = _rows(G, T, seed, j, prec)
                 else:
