@@ -113,6 +113,10 @@ typedef struct {
     void *row_values;         /* optional device array[n]: per-vertex Σ_C M_0(i,I_C)
                                  of the LAST colouring of the call (double for
                                  F32/F64, uint64 for U64)                            */
+    int32_t layout;           /* count-table layout: 0 = root-colour anchored
+                                 (default; rows hold only colour sets containing
+                                 c(i), C(k-1,s-1) columns),
+                                 1 = dense n x C(k,s) as in P:227.  Same results. */
 } sg2v_options;
 
 void sg2v_options_default(sg2v_options *o);
@@ -120,7 +124,9 @@ void sg2v_options_default(sg2v_options *o);
 sg2v_status sg2v_set_options(const sg2v_options *o);
 
 /* Device bytes sg2v_count needs for (g, t, precision): all count tables live
- * at the peak of the planned schedule + colours + histogram + row values. */
+ * at the peak of the planned schedule + colours + histogram + row values.
+ * sg2v_workspace_bytes and sg2v_plan_describe* plan for the layout of the
+ * thread-local options (sg2v_set_options). */
 sg2v_status sg2v_workspace_bytes(const sg2v_graph *g, const sg2v_template *t,
                                  sg2v_precision precision, uint64_t *bytes);
 

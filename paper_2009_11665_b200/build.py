@@ -14,8 +14,8 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIBDIR = os.path.join(PKG, "lib")
 LIB = os.path.join(LIBDIR, "libsg2v.so")
-SOURCES = ["api.cpp", "planner.cpp", "kernels.cu"]
-HEADERS = ["sg2v_internal.h", os.path.join("..", "..", "include", "sg2v.h")]
+SOURCES = ["api.cpp", "planner.cpp", "kernels.cu", "akernels.cu"]
+HEADERS = ["sg2v_internal.h", "kcommon.cuh", os.path.join("..", "..", "include", "sg2v.h")]
 
 
 def nvcc() -> str:

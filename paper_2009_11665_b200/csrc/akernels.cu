@@ -1,0 +1,379 @@
+// akernels.cu — root-colour-anchored kernels.
+//
+// A table row of vertex i for a sub-template of size s stores only the colour
+// sets S ∋ c(i): M_s(i,S) = 0 whenever c(i) ∉ S (the root is mapped to i), so the
+// row is indexed by S∖{c(i)} relabelled into [k-1] (colex rank), C(k-1,s-1)
+// columns instead of C(k,s).  The DP of Alg. 3 is unchanged:
+//   B(i,T)   = Σ_{j∈N(i)} M_p(j,T)             only T ∌ c(i) are ever used, and
+//              only neighbours with c(j) ∈ T contribute: grouping N(i) by colour x,
+//            = Σ_{x∈T} R_x(T∖{x}),  R_x = Σ_{j∈N(i), c(j)=x} M_p(j,·)      (a4)
+//   M_s(i,S) = Σ_{S_a} M_a(i,S_a)·B(i,S∖S_a)  over the universe [k-1] with one
+//              split table for every vertex; = B(i,·) itself when |T_a| = 1   (a5)
+// Monochromatic edges (c(j) = c(i)) contribute nothing and are skipped.
+//
+//  bucket_kernel  per colouring: colour counts H(i,x) and a colour-bucketed copy
+//                 of every CSR row (stable), one warp per row
+//  astep_kernel   fused gather (per-colour register sums R_x, pushed into B in
+//                 shared memory through the [x][c(i)] map) + eMA + store
+//  atop_leaf_kernel  top step with a leaf active child: one column per edge
+#include <cuda_runtime.h>
+
+#include "kcommon.cuh"
+#include "sg2v_internal.h"
+
+namespace sg2v {
+
+__device__ __forceinline__ unsigned lanemask_lt() {
+    unsigned m;
+    asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+    return m;
+}
+
+// ---------------------------------------------------------------------------
+// colour counts + colour-bucketed CSR (stable within each colour)
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) bucket_kernel(int64_t n, int k, int kp, const int64_t *__restrict__ rowptr,
+                                                     const int32_t *__restrict__ col,
+                                                     const uint8_t *__restrict__ colors,
+                                                     int32_t *__restrict__ hcnt, int32_t *__restrict__ bcol) {
+    const int lane = threadIdx.x & 31;
+    const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+    for (int64_t i = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); i < n; i += warps) {
+        const int64_t e0 = rowptr[i], e1 = rowptr[i + 1];
+        int cnt = 0;  // lane x: neighbours of colour x
+        for (int64_t base = e0; base < e1; base += 32) {
+            const int64_t e = base + lane;
+            const int c = (e < e1) ? (int)colors[__ldg(col + e)] : 255;
+            for (int x = 0; x < k; ++x) {
+                const unsigned b = __ballot_sync(0xffffffffu, c == x);
+                if (lane == x) cnt += __popc(b);
+            }
+        }
+        if (lane < kp) hcnt[i * kp + lane] = (lane < k) ? cnt : 0;
+        // exclusive scan over colours -> start of each colour's bucket
+        int incl = (lane < k) ? cnt : 0;
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, incl, off);
+            if (lane >= off) incl += y;
+        }
+        int run = incl - ((lane < k) ? cnt : 0);
+        for (int64_t base = e0; base < e1; base += 32) {
+            const int64_t e = base + lane;
+            const int32_t j = (e < e1) ? __ldg(col + e) : 0;
+            const int c = (e < e1) ? (int)colors[j] : 255;
+            const unsigned m = __match_any_sync(0xffffffffu, c);
+            const int pos = __shfl_sync(0xffffffffu, run, c & 31) + __popc(m & lanemask_lt());
+            if (e < e1) bcol[e0 + pos] = j;
+            for (int x = 0; x < k; ++x) {
+                const unsigned b = __ballot_sync(0xffffffffu, c == x);
+                if (lane == x) run += __popc(b);
+            }
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// fused anchored step
+// ---------------------------------------------------------------------------
+struct AStepArgs {
+    int64_t n;
+    int k, kp;
+    const int64_t *rowptr;
+    const int32_t *bcol;
+    const int32_t *hcnt;
+    const int32_t *order;
+    const uint8_t *colors;
+    const char *mp;     // passive anchored table (gather source)
+    int64_t ldp, cp;    // its row stride / width C(k-1,p-1)
+    int src_hist;       // p = 1: B(i,{y}) = H(i,y)
+    const int32_t *pmap;  // push map [x][c(i)][cp] -> B column or -1
+    const char *ma;     // active anchored table (GENERAL)
+    int64_t lda;
+    char *ms;           // output table (non-top)
+    int64_t lds, cs;
+    int64_t ldb, cb;    // B row: C(k-1,p) columns
+    int comb, top;
+    const int32_t *idx; // GENERAL split pairs over [k-1]
+    int64_t nterms;
+    void *rowval;
+    int64_t smem_group;
+};
+
+template <typename T, typename RT, int GT>
+__global__ void __launch_bounds__(256) astep_kernel(AStepArgs A) {
+    constexpr int G = 256 / GT;
+    constexpr int VN = Vec<T>::N;
+    constexpr int R = 4;
+    constexpr int U = 4;
+    extern __shared__ __align__(16) unsigned char smem[];
+    __shared__ RT red[8];
+    const int g = threadIdx.x / GT, t = threadIdx.x % GT;
+    T *sB = reinterpret_cast<T *>(smem) + (size_t)g * A.smem_group;
+    T *sA = sB + A.ldb;
+    const int64_t nslots = (A.n + G - 1) / G;
+    const int64_t nvec_p = A.ldp / VN;
+    const size_t row_bytes = (size_t)A.ldp * sizeof(T);
+    const int k = A.k;
+
+    for (int64_t slot = blockIdx.x; slot < nslots; slot += gridDim.x) {
+        const int64_t r = slot * G + g;
+        const bool act = r < A.n;
+        const int64_t i = act ? A.order[r] : 0;
+        const int ci = act ? (int)A.colors[i] : 0;
+        if (act) {
+            for (int64_t v = t; v < A.ldb / VN; v += GT) reinterpret_cast<uint4 *>(sB)[v] = make_uint4(0, 0, 0, 0);
+            if (A.comb == COMB_GENERAL) {
+                const char *a = A.ma + (size_t)i * A.lda * sizeof(T);
+                for (int64_t v = t; v < A.lda / VN; v += GT) reinterpret_cast<uint4 *>(sA)[v] = ldg16(a + v * 16);
+            }
+        }
+        group_sync<GT>(g);
+        // ---- stage 1: B(i,·) over T ⊂ [k]∖{c(i)} ------------------------------
+        if (act) {
+            const int32_t *h = A.hcnt + (size_t)i * A.kp;
+            if (A.src_hist) {
+                for (int64_t y = t; y < A.cb; y += GT) sB[y] = (T)__ldg(h + y + (y >= ci ? 1 : 0));
+            } else {
+                int64_t e = A.rowptr[i];
+                for (int x = 0; x < k; ++x) {
+                    const int cnt = __ldg(h + x);
+                    if (x != ci && cnt > 0) {
+                        const int32_t *mp = A.pmap + ((size_t)x * k + ci) * A.cp;
+                        for (int64_t v0 = 0; v0 < nvec_p; v0 += GT * R) {
+                            uint4 acc[R];
+#pragma unroll
+                            for (int q = 0; q < R; ++q) acc[q] = make_uint4(0, 0, 0, 0);
+                            int64_t e2 = e;
+                            const int64_t e3 = e + cnt;
+                            for (; e2 + U <= e3; e2 += U) {
+                                int32_t jj[U];
+#pragma unroll
+                                for (int u = 0; u < U; ++u) jj[u] = __ldg(A.bcol + e2 + u);
+                                uint4 xv[U][R];
+#pragma unroll
+                                for (int u = 0; u < U; ++u)
+#pragma unroll
+                                    for (int q = 0; q < R; ++q) {
+                                        const int64_t v = v0 + q * GT + t;
+                                        xv[u][q] = (v < nvec_p) ? ldg16(A.mp + (size_t)jj[u] * row_bytes + v * 16)
+                                                                : make_uint4(0, 0, 0, 0);
+                                    }
+#pragma unroll
+                                for (int u = 0; u < U; ++u)
+#pragma unroll
+                                    for (int q = 0; q < R; ++q) Vec<T>::add(acc[q], xv[u][q]);
+                            }
+                            for (; e2 < e3; ++e2) {
+                                const int32_t j1 = __ldg(A.bcol + e2);
+#pragma unroll
+                                for (int q = 0; q < R; ++q) {
+                                    const int64_t v = v0 + q * GT + t;
+                                    if (v < nvec_p) Vec<T>::add(acc[q], ldg16(A.mp + (size_t)j1 * row_bytes + v * 16));
+                                }
+                            }
+                            // push R_x into B: distinct targets within one colour
+#pragma unroll
+                            for (int q = 0; q < R; ++q) {
+                                const int64_t v = v0 + q * GT + t;
+                                if (v < nvec_p) {
+#pragma unroll
+                                    for (int el = 0; el < VN; ++el) {
+                                        const int64_t u = v * VN + el;
+                                        if (u < A.cp) {
+                                            const int32_t tt = __ldg(mp + u);
+                                            if (tt >= 0) sB[tt] += vget<T>(acc[q], el);
+                                        }
+                                    }
+                                }
+                            }
+                        }
+                        group_sync<GT>(g);  // colours x and x' may push to the same T
+                    }
+                    e += cnt;
+                }
+            }
+        }
+        group_sync<GT>(g);
+        // ---- stage 2: eMA over the universe [k-1] ------------------------------
+        RT racc = 0;
+        if (act) {
+            if (!A.top) {
+                T *out = reinterpret_cast<T *>(A.ms) + (size_t)i * A.lds;
+                if (A.comb == COMB_ACTIVE_LEAF) {
+                    // M_s(i,·) = B(i,·): |T_s| - 1 = |T_p| and the colour sets coincide
+                    for (int64_t v = t; v < A.lds / VN; v += GT)
+                        reinterpret_cast<uint4 *>(out)[v] = reinterpret_cast<const uint4 *>(sB)[v];
+                } else {
+                    const int2 *sp = reinterpret_cast<const int2 *>(A.idx);
+                    for (int64_t o = t; o < A.lds; o += GT) {
+                        T acc = 0;
+                        if (o < A.cs) {
+                            const int2 *p = sp + (size_t)o * A.nterms;
+                            for (int64_t w = 0; w < A.nterms; ++w) {
+                                const int2 q = __ldg(p + w);
+                                acc += sA[q.x] * sB[q.y];
+                            }
+                        }
+                        out[o] = acc;
+                    }
+                }
+            } else {
+                const int2 *sp = reinterpret_cast<const int2 *>(A.idx);
+                for (int64_t w = t; w < A.nterms; w += GT) {
+                    const int2 q = __ldg(sp + w);
+                    racc += (RT)sA[q.x] * (RT)sB[q.y];
+                }
+            }
+        }
+        if (A.top) {
+            RT s = group_reduce<RT, GT>(racc, g, red);
+            if (act && t == 0) reinterpret_cast<RT *>(A.rowval)[i] = s;
+        }
+        group_sync<GT>(g);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// top step, leaf active child: colorful_i = Σ_{j∈N(i), c(j)≠c(i)} M_p(j, topcol[c(j)][c(i)])
+// ---------------------------------------------------------------------------
+template <typename T, typename RT>
+__global__ void __launch_bounds__(256) atop_leaf_kernel(int64_t n, int k, int kp, const int64_t *__restrict__ rowptr,
+                                                        const int32_t *__restrict__ col,
+                                                        const uint8_t *__restrict__ colors,
+                                                        const int32_t *__restrict__ hcnt, const T *__restrict__ src,
+                                                        int64_t ldp, int src_hist, const int32_t *__restrict__ topcol,
+                                                        RT *__restrict__ rowval) {
+    const int lane = threadIdx.x & 31;
+    const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+    for (int64_t i = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); i < n; i += warps) {
+        const int ci = colors[i];
+        RT acc = 0;
+        if (src_hist) {  // k = 2: the one other colour
+            if (lane == 0) acc = (RT)hcnt[(size_t)i * kp + (ci == 0 ? 1 : 0)];
+        } else {
+            const int64_t e0 = rowptr[i], e1 = rowptr[i + 1];
+            for (int64_t e = e0 + lane; e < e1; e += 32) {
+                const int32_t j = __ldg(col + e);
+                const int cj = colors[j];
+                if (cj != ci) acc += (RT)__ldg(src + (size_t)j * ldp + __ldg(topcol + cj * k + ci));
+            }
+#pragma unroll
+            for (int off = 16; off > 0; off >>= 1) acc += __shfl_down_sync(0xffffffffu, acc, off);
+        }
+        if (lane == 0) rowval[i] = acc;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// launchers
+// ---------------------------------------------------------------------------
+int launch_bucket(const Graph &g, const Plan &pl, const uint8_t *colors, int32_t *hcnt, int32_t *bcol,
+                  void *stream) {
+    if (g.n <= 0) return 0;
+    int64_t blocks = std::min<int64_t>((g.n + 7) / 8, (int64_t)num_sms() * 8);
+    double bytes = g.nnz * 9.0 + g.nnz * 4.0 + g.n * 16.0 + (double)g.n * pl.kp * 4.0;
+    prof_begin(1, stream);
+    bucket_kernel<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(g.n, pl.k, (int)pl.kp, g.d_rowptr, g.d_col,
+                                                                      colors, hcnt, bcol);
+    prof_end(1, bytes, stream);
+    return (int)cudaGetLastError();
+}
+
+template <typename T, typename RT, int GT>
+static int launch_astep_t(const AStepArgs &A, void *stream) {
+    auto kern = astep_kernel<T, RT, GT>;
+    constexpr int G = 256 / GT;
+    size_t smem = (size_t)G * A.smem_group * sizeof(T);
+    if (smem > 227 * 1024) return -1;
+    static size_t configured = 0;
+    if (smem > 48 * 1024 && smem > configured) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return (int)e;
+        configured = smem;
+    }
+    int occ = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 256, smem);
+    if (occ < 1) occ = 1;
+    int64_t nslots = (A.n + G - 1) / G;
+    int64_t blocks = std::min<int64_t>(nslots, (int64_t)occ * num_sms());
+    if (blocks < 1) blocks = 1;
+    kern<<<(unsigned)blocks, 256, smem, (cudaStream_t)stream>>>(A);
+    return (int)cudaGetLastError();
+}
+
+template <typename T, typename RT>
+static int launch_astep_gt(const AStepArgs &A, int gt, void *stream) {
+    switch (gt) {
+        case 4: return launch_astep_t<T, RT, 4>(A, stream);
+        case 8: return launch_astep_t<T, RT, 8>(A, stream);
+        case 16: return launch_astep_t<T, RT, 16>(A, stream);
+        case 32: return launch_astep_t<T, RT, 32>(A, stream);
+        case 64: return launch_astep_t<T, RT, 64>(A, stream);
+        case 128: return launch_astep_t<T, RT, 128>(A, stream);
+        default: return launch_astep_t<T, RT, 256>(A, stream);
+    }
+}
+
+int launch_astep(const Graph &g, const Plan &pl, const Step &st, const uint8_t *colors, const int32_t *hcnt,
+                 const int32_t *bcol, char *tables, void *rowval, void *stream) {
+    if (g.n <= 0) return 0;
+    const int32_t *idx = pl.d_index + st.idx_off;
+    const char *src = (st.src == SRC_HIST) ? nullptr : tables + pl.bufs[st.buf_p].offset;
+    if (st.top && st.comb == COMB_ACTIVE_LEAF) {
+        int64_t blocks = std::min<int64_t>((g.n + 7) / 8, (int64_t)num_sms() * 8);
+        int srch = st.src == SRC_HIST;
+        prof_begin(3, stream);
+        if (pl.prec == SG2V_F32)
+            atop_leaf_kernel<float, double><<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(
+                g.n, pl.k, (int)pl.kp, g.d_rowptr, g.d_col, colors, hcnt, (const float *)src, st.ldp, srch, idx,
+                (double *)rowval);
+        else if (pl.prec == SG2V_F64)
+            atop_leaf_kernel<double, double><<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(
+                g.n, pl.k, (int)pl.kp, g.d_rowptr, g.d_col, colors, hcnt, (const double *)src, st.ldp, srch, idx,
+                (double *)rowval);
+        else
+            atop_leaf_kernel<u64, u64><<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(
+                g.n, pl.k, (int)pl.kp, g.d_rowptr, g.d_col, colors, hcnt, (const u64 *)src, st.ldp, srch, idx,
+                (u64 *)rowval);
+        prof_end(3, st.alg_bytes, stream);
+        return (int)cudaGetLastError();
+    }
+    AStepArgs A;
+    A.n = g.n;
+    A.k = pl.k;
+    A.kp = (int)pl.kp;
+    A.rowptr = g.d_rowptr;
+    A.bcol = bcol;
+    A.hcnt = hcnt;
+    A.order = g.d_order;
+    A.colors = colors;
+    A.mp = src;
+    A.ldp = st.ldp;
+    A.cp = st.cp;
+    A.src_hist = st.src == SRC_HIST;
+    A.pmap = st.map_off >= 0 ? pl.d_index + st.map_off : nullptr;
+    A.ma = (st.comb == COMB_GENERAL) ? tables + pl.bufs[st.buf_a].offset : nullptr;
+    A.lda = st.lda;
+    A.ms = st.top ? nullptr : tables + pl.bufs[st.buf_out].offset;
+    A.lds = st.lds;
+    A.cs = st.cs;
+    A.ldb = st.ldb;
+    A.cb = st.cb;
+    A.comb = st.comb;
+    A.top = st.top;
+    A.idx = idx;
+    A.nterms = st.nterms;
+    A.rowval = rowval;
+    A.smem_group = st.ldb + (st.comb == COMB_GENERAL ? st.lda : 0);
+    int cls = st.top ? 3 : 2;
+    prof_begin(cls, stream);
+    int rc;
+    if (pl.prec == SG2V_F32) rc = launch_astep_gt<float, double>(A, st.gt, stream);
+    else if (pl.prec == SG2V_F64) rc = launch_astep_gt<double, double>(A, st.gt, stream);
+    else rc = launch_astep_gt<u64, u64>(A, st.gt, stream);
+    prof_end(cls, st.alg_bytes, stream);
+    return rc;
+}
+
+}  // namespace sg2v

@@ -102,13 +102,18 @@ static sg2v_status ensure_device(int dev) {
 
 // Plans are cached per (precision, n, nnz, device); the index tables are
 // uploaded lazily, so planning itself needs no GPU (host-only tests use it).
+static Layout current_layout(int32_t lay) { return lay == 1 ? LAYOUT_DENSE : LAYOUT_ANCHORED; }
+
+static int32_t tls_layout() { return g_opts_init ? g_opts.layout : 0; }
+
 static sg2v_status get_plan(int64_t n, int64_t nnz, int device, const Template &t, sg2v_precision prec,
-                            bool upload, Plan **out) {
-    auto key = std::make_tuple((int)prec, n, nnz, device);
+                            int32_t layout, bool upload, Plan **out) {
+    if (layout != 0 && layout != 1) { set_error("layout must be 0 (anchored) or 1 (dense)"); return SG2V_EINVAL; }
+    auto key = std::make_tuple((int)prec, n, nnz, device, (int)layout);
     auto &slot = const_cast<Template &>(t).plans[key];
     if (!slot) {
         std::unique_ptr<Plan> pl;
-        sg2v_status st = make_plan(t, n, nnz, prec, pl);
+        sg2v_status st = make_plan(t, n, nnz, prec, current_layout(layout), pl);
         if (st != SG2V_OK) return st;
         slot = std::move(pl);
     }
@@ -251,7 +256,7 @@ sg2v_status sg2v_workspace_bytes(const sg2v_graph *g, const sg2v_template *t, sg
     if (prec < SG2V_F32 || prec > SG2V_U64) { set_error("bad precision"); return SG2V_EINVAL; }
     if (t->k == 1 || g->n == 0) { *bytes = 0; return SG2V_OK; }
     Plan *pl = nullptr;
-    sg2v_status st = get_plan(g->n, g->nnz, g->device, *t, prec, false, &pl);
+    sg2v_status st = get_plan(g->n, g->nnz, g->device, *t, prec, tls_layout(), false, &pl);
     if (st != SG2V_OK) return st;
     *bytes = (uint64_t)pl->ws_bytes;
     return SG2V_OK;
@@ -272,7 +277,7 @@ sg2v_status sg2v_plan_describe_n(int64_t n, int64_t nnz, const sg2v_template *t,
         s = "{\"k\":" + std::to_string(t->k) + ",\"steps\":[],\"workspace_bytes\":0,\"alg_bytes\":0}";
     } else {
         Plan *pl = nullptr;
-        sg2v_status st = get_plan(n, nnz, -1, *t, prec, false, &pl);
+        sg2v_status st = get_plan(n, nnz, -1, *t, prec, tls_layout(), false, &pl);
         if (st != SG2V_OK) return st;
         s = pl->describe();
     }
@@ -325,7 +330,7 @@ sg2v_status sg2v_count_ex(const sg2v_graph *g, const sg2v_template *t, int32_t k
         }
     } else {
         Plan *pl = nullptr;
-        st = get_plan(g->n, g->nnz, g->device, *t, o.precision, true, &pl);
+        st = get_plan(g->n, g->nnz, g->device, *t, o.precision, o.layout, true, &pl);
         if (st != SG2V_OK) return st;
         char *ws = (char *)o.workspace;
         bool own = false;
@@ -357,6 +362,9 @@ sg2v_status sg2v_count_ex(const sg2v_graph *g, const sg2v_template *t, int32_t k
         void *rowval = ws + pl->off_rowval;
         void *partial = ws + pl->off_partial;
         char *results = ws + pl->off_results;
+        int32_t *hcnt = (int32_t *)(ws + pl->off_hcnt);
+        int32_t *bcol = (int32_t *)(ws + pl->off_bcol);
+        const bool anch = pl->layout == LAYOUT_ANCHORED;
         std::vector<uint64_t> host_ring(kResultsRing);
         int64_t base = 0;
         for (int64_t q = 0; q < n_iter; ++q) {
@@ -364,8 +372,10 @@ sg2v_status sg2v_count_ex(const sg2v_graph *g, const sg2v_template *t, int32_t k
             int rc = launch_colorize(seed, j, g->n, k, colors, s);
             if (rc) return cuda_fail("colorize", rc);
             if (pl->need_hist && (rc = launch_hist(*g, *pl, colors, H, s))) return cuda_fail("hist", rc);
+            if (anch && (rc = launch_bucket(*g, *pl, colors, hcnt, bcol, s))) return cuda_fail("bucket", rc);
             for (const Step &stp : pl->steps) {
-                rc = launch_step(*g, *pl, stp, colors, H, ws, rowval, s);
+                rc = anch ? launch_astep(*g, *pl, stp, colors, hcnt, bcol, ws, rowval, s)
+                          : launch_step(*g, *pl, stp, colors, H, ws, rowval, s);
                 if (rc == -1) {
                     set_error("row too wide for on-chip B (shared memory > 227 KB)");
                     return SG2V_ENOMEM;

@@ -1,0 +1,100 @@
+// kcommon.cuh — device helpers shared by the dense (kernels.cu) and the
+// root-colour-anchored (akernels.cu) kernels.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+namespace sg2v {
+
+typedef unsigned long long u64;
+
+// 16-byte vector arithmetic on raw uint4 bits, per element type
+template <typename T> struct Vec;
+template <> struct Vec<float> {
+    static constexpr int N = 4;
+    __device__ __forceinline__ static void add(uint4 &a, const uint4 &b) {
+        a.x = __float_as_uint(__uint_as_float(a.x) + __uint_as_float(b.x));
+        a.y = __float_as_uint(__uint_as_float(a.y) + __uint_as_float(b.y));
+        a.z = __float_as_uint(__uint_as_float(a.z) + __uint_as_float(b.z));
+        a.w = __float_as_uint(__uint_as_float(a.w) + __uint_as_float(b.w));
+    }
+};
+template <> struct Vec<double> {
+    static constexpr int N = 2;
+    __device__ __forceinline__ static void add(uint4 &a, const uint4 &b) {
+        double2 x = *reinterpret_cast<double2 *>(&a);
+        const double2 y = *reinterpret_cast<const double2 *>(&b);
+        x.x += y.x;
+        x.y += y.y;
+        a = *reinterpret_cast<uint4 *>(&x);
+    }
+};
+template <> struct Vec<u64> {
+    static constexpr int N = 2;
+    __device__ __forceinline__ static void add(uint4 &a, const uint4 &b) {
+        ulonglong2 x = *reinterpret_cast<ulonglong2 *>(&a);
+        const ulonglong2 y = *reinterpret_cast<const ulonglong2 *>(&b);
+        x.x += y.x;  // wraps mod 2^64 (exact residue arithmetic)
+        x.y += y.y;
+        a = *reinterpret_cast<uint4 *>(&x);
+    }
+};
+
+// read-only 128-bit load through the non-coherent path
+__device__ __forceinline__ uint4 ldg16(const void *p) {
+    uint4 r;
+    asm volatile("ld.global.nc.v4.u32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+                 : "l"(p));
+    return r;
+}
+
+// Synchronise the GT threads of row group g (GT | 256).  Groups narrower than a
+// warp sync only their own lanes, so the call is legal inside group-uniform
+// (but warp-divergent) control flow.
+template <int GT>
+__device__ __forceinline__ void group_sync(int g) {
+    if constexpr (GT < 32) {
+        const unsigned lane = threadIdx.x & 31u;
+        const unsigned mask = ((1u << GT) - 1u) << (lane & ~(unsigned)(GT - 1));
+        __syncwarp(mask);
+    } else if constexpr (GT == 32) {
+        __syncwarp();
+    } else if constexpr (GT == 256) {
+        __syncthreads();
+    } else {
+        asm volatile("bar.sync %0, %1;" ::"r"(g + 1), "r"(GT) : "memory");
+    }
+}
+
+// Sum over the GT threads of group g (must be called by every thread of the
+// block, in uniform control flow).  Result valid in the group's thread 0.
+template <typename RT, int GT>
+__device__ __forceinline__ RT group_reduce(RT v, int g, RT *red) {
+    const int lane = threadIdx.x & 31;
+    constexpr int W = GT < 32 ? GT : 32;
+#pragma unroll
+    for (int off = W / 2; off > 0; off >>= 1) v += __shfl_down_sync(0xffffffffu, v, off, W);
+    if constexpr (GT > 32) {
+        const int warp = threadIdx.x >> 5;
+        if (lane == 0) red[warp] = v;
+        group_sync<GT>(g);
+        RT s = 0;
+        if ((threadIdx.x % GT) == 0)
+            for (int w = 0; w < GT / 32; ++w) s += red[g * (GT / 32) + w];
+        return s;
+    } else {
+        return v;
+    }
+}
+
+// element e (0..VN-1) of a 16-B vector as T
+template <typename T>
+__device__ __forceinline__ T vget(const uint4 &v, int e) {
+    return reinterpret_cast<const T *>(&v)[e];
+}
+
+int num_sms();
+
+}  // namespace sg2v

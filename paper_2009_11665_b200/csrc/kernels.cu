@@ -20,53 +20,10 @@
 
 #include <cstdio>
 
+#include "kcommon.cuh"
 #include "sg2v_internal.h"
 
 namespace sg2v {
-
-typedef unsigned long long u64;
-
-// ---------------------------------------------------------------------------
-// 16-byte vector arithmetic on raw uint4 bits, per element type
-// ---------------------------------------------------------------------------
-template <typename T> struct Vec;
-template <> struct Vec<float> {
-    static constexpr int N = 4;
-    __device__ __forceinline__ static void add(uint4 &a, const uint4 &b) {
-        a.x = __float_as_uint(__uint_as_float(a.x) + __uint_as_float(b.x));
-        a.y = __float_as_uint(__uint_as_float(a.y) + __uint_as_float(b.y));
-        a.z = __float_as_uint(__uint_as_float(a.z) + __uint_as_float(b.z));
-        a.w = __float_as_uint(__uint_as_float(a.w) + __uint_as_float(b.w));
-    }
-};
-template <> struct Vec<double> {
-    static constexpr int N = 2;
-    __device__ __forceinline__ static void add(uint4 &a, const uint4 &b) {
-        double2 x = *reinterpret_cast<double2 *>(&a);
-        const double2 y = *reinterpret_cast<const double2 *>(&b);
-        x.x += y.x;
-        x.y += y.y;
-        a = *reinterpret_cast<uint4 *>(&x);
-    }
-};
-template <> struct Vec<u64> {
-    static constexpr int N = 2;
-    __device__ __forceinline__ static void add(uint4 &a, const uint4 &b) {
-        ulonglong2 x = *reinterpret_cast<ulonglong2 *>(&a);
-        const ulonglong2 y = *reinterpret_cast<const ulonglong2 *>(&b);
-        x.x += y.x;  // wraps mod 2^64 (exact residue arithmetic)
-        x.y += y.y;
-        a = *reinterpret_cast<uint4 *>(&x);
-    }
-};
-
-__device__ __forceinline__ uint4 ldg16(const void *p) {
-    uint4 r;
-    asm volatile("ld.global.nc.v4.u32 {%0,%1,%2,%3}, [%4];"
-                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
-                 : "l"(p));
-    return r;
-}
 
 // ---------------------------------------------------------------------------
 // a1: colouring (SURVEY §8(c) step 1 counter hash; bias <= k/2^32)
@@ -136,36 +93,6 @@ struct StepArgs {
     void *rowval;      // top: per-vertex values (RT)
     int64_t smem_group;  // elements of shared memory per row group
 };
-
-template <int GT>
-__device__ __forceinline__ void group_sync(int g) {
-    if constexpr (GT <= 32) {
-        __syncwarp();
-    } else if constexpr (GT == 256) {
-        __syncthreads();
-    } else {
-        asm volatile("bar.sync %0, %1;" ::"r"(g + 1), "r"(GT) : "memory");
-    }
-}
-
-template <typename RT, int GT>
-__device__ __forceinline__ RT group_reduce(RT v, int g, RT *red) {
-    const int lane = threadIdx.x & 31;
-    constexpr int W = GT < 32 ? GT : 32;
-#pragma unroll
-    for (int off = W / 2; off > 0; off >>= 1) v += __shfl_down_sync(0xffffffffu, v, off, W);
-    if constexpr (GT > 32) {
-        const int warp = threadIdx.x >> 5;
-        if (lane == 0) red[warp] = v;
-        group_sync<GT>(g);
-        RT s = 0;
-        if ((threadIdx.x % GT) == 0)
-            for (int w = 0; w < GT / 32; ++w) s += red[g * (GT / 32) + w];
-        return s;
-    } else {
-        return v;
-    }
-}
 
 template <typename T, typename RT, int GT>
 __global__ void __launch_bounds__(256) step_kernel(StepArgs A) {
@@ -379,7 +306,7 @@ __global__ void validate_kernel(int64_t n, int64_t nnz, const int64_t *__restric
 // ---------------------------------------------------------------------------
 // launchers
 // ---------------------------------------------------------------------------
-static int num_sms() {
+int num_sms() {
     static int sms = 0;
     if (!sms) {
         int dev = 0;

@@ -198,28 +198,42 @@ static int pick_gt(int64_t cols, int vn) {
     return gt;
 }
 
+
 static constexpr double kHbm = 6.5e12;     // B/s, MEASURED_PEAKS hbm_gbs (planning only)
 static constexpr double kTermRate = 2.0e12; // eMA terms/s (smem-bound estimate)
 
+// Relabelling of colour sets for the root-colour-anchored layout:
+// a set over [k] \ {e} is stored as a set over [k-1] by closing the gap at e.
+static uint32_t drop_bit(uint32_t m, int e) { return ((m >> (e + 1)) << e) | (m & ((1u << e) - 1)); }
+static uint32_t insert_gap(uint32_t m, int e) { return ((m >> e) << (e + 1)) | (m & ((1u << e) - 1)); }
+
+// Row width of a count table for a node of `size` vertices.
+static int64_t table_width(Layout L, int k, int size) {
+    return L == LAYOUT_DENSE ? binom(k, size) : binom(k - 1, size - 1);
+}
+
 // Build steps, schedule, buffers and the model for one chain.
 static bool plan_chain(const Template &t, const Chain &c, int root, int64_t n, int64_t nnz,
-                       sg2v_precision prec, Plan &pl) {
+                       sg2v_precision prec, Layout L, Plan &pl) {
     const int k = t.k;
     pl = Plan();
     pl.k = k;
     pl.root = root;
     pl.prec = prec;
+    pl.layout = L;
     pl.elem = (prec == SG2V_F32) ? 4 : 8;
     const int vn = 16 / pl.elem;
     pl.nodes = c.nodes;
     const double E = pl.elem;
+    const bool anch = (L == LAYOUT_ANCHORED);
+    const double live_frac = anch ? (double)(k - 1) / k : 1.0;  // non-monochromatic edges (expected)
 
     // --- children-first order minimising the peak (Sethi–Ullman style) ---
     std::vector<int64_t> out_bytes(pl.nodes.size(), 0);
     for (size_t i = 0; i < pl.nodes.size(); ++i) {
         const Node &nd = pl.nodes[i];
         if (nd.active >= 0 && (int)i != c.top)
-            out_bytes[i] = n * round_up(binom(k, nd.size), vn) * pl.elem;
+            out_bytes[i] = n * round_up(table_width(L, k, nd.size), vn) * pl.elem;
     }
     std::vector<int> sched;
     std::function<int64_t(int, std::vector<int> &)> order = [&](int v, std::vector<int> &seq) -> int64_t {
@@ -244,7 +258,7 @@ static bool plan_chain(const Template &t, const Chain &c, int root, int64_t n, i
 
     // --- first-fit arena over the schedule ---
     std::vector<int> node_buf(pl.nodes.size(), -1);
-    std::vector<std::pair<int64_t, int64_t>> live;  // (offset, bytes) sorted by offset
+    std::vector<std::pair<int64_t, int64_t>> live;  // (offset, bytes)
     int64_t arena = 0;
     auto alloc = [&](int64_t bytes) -> int64_t {
         int64_t pos = 0;
@@ -274,15 +288,17 @@ static bool plan_chain(const Template &t, const Chain &c, int root, int64_t n, i
         st.top = (v == c.top);
         st.src = (st.p == 1) ? SRC_HIST : SRC_GATHER;
         st.comb = (st.a == 1) ? COMB_ACTIVE_LEAF : COMB_GENERAL;
-        st.cs = st.top ? 1 : binom(k, st.s);
-        st.ca = binom(k, st.a);
-        st.cp = binom(k, st.p);
+        st.cs = st.top ? 1 : table_width(L, k, st.s);
+        st.ca = table_width(L, k, st.a);
+        st.cp = table_width(L, k, st.p);
+        st.cb = anch ? binom(k - 1, st.p) : st.cp;
         st.lds = st.top ? 1 : round_up(st.cs, vn);
         st.lda = round_up(st.ca, vn);
         st.ldp = (st.src == SRC_HIST) ? round_up(k, vn) : round_up(st.cp, vn);
+        st.ldb = anch ? round_up(st.cb, vn) : st.ldp;
         st.buf_a = node_buf[nd.active];
         st.buf_p = node_buf[nd.passive];
-        if (st.src == SRC_HIST) pl.need_hist = true;
+        if (st.src == SRC_HIST && !anch) pl.need_hist = true;
         if (!st.top) {
             Buffer b;
             b.bytes = n * st.lds * pl.elem;
@@ -297,38 +313,53 @@ static bool plan_chain(const Template &t, const Chain &c, int root, int64_t n, i
         // algorithmic bytes (useful columns only) and the model (sector-rounded)
         double bytes = 0.0, mbytes = 0.0;
         const bool top_leaf = st.top && st.comb == COMB_ACTIVE_LEAF;
+        const double hsrc = anch ? n * (double)round_up(k, 4) * 4.0 : n * (double)k * E;
         if (top_leaf) {
             if (st.src == SRC_GATHER) {
-                bytes = nnz * 4.0 + nnz * E + n * 9.0;
-                mbytes = nnz * 4.0 + nnz * 32.0 + n * 16.0;
+                bytes = nnz * 4.0 + nnz * live_frac * E + n * 9.0;
+                mbytes = nnz * 4.0 + nnz * live_frac * 32.0 + n * 16.0;
             } else {
-                bytes = mbytes = n * (E + 9.0);
+                bytes = mbytes = hsrc + n * 9.0;
             }
         } else {
-            double gather = (st.src == SRC_GATHER) ? nnz * 4.0 + nnz * (double)st.cp * E + n * 12.0
-                                                   : n * (double)k * E;
-            double mg = (st.src == SRC_GATHER) ? nnz * 4.0 + nnz * (double)round_up(st.cp * pl.elem, 32) + n * 12.0
-                                               : n * (double)st.ldp * E;
+            double gather = (st.src == SRC_GATHER)
+                                ? nnz * 4.0 + nnz * live_frac * (double)st.cp * E + n * (12.0 + (anch ? 4.0 * k : 0.0))
+                                : hsrc;
+            double mg = (st.src == SRC_GATHER)
+                            ? nnz * 4.0 + nnz * live_frac * (double)round_up(st.cp * pl.elem, 32) + n * 12.0
+                            : hsrc;
             double ma = (st.comb == COMB_GENERAL) ? n * (double)st.ca * E : n * 1.0;
             double w = st.top ? n * 8.0 : n * (double)st.cs * E;
             bytes = gather + ma + w;
             mbytes = mg + ma + w;
+            if (anch && st.src == SRC_GATHER)  // per-row push of k-1 colour partial sums through smem
+                mbytes += n * (double)(k - 1) * (double)st.cp * 4.0 * 0.1;
         }
-        st.nterms = (st.comb == COMB_GENERAL) ? (st.top ? binom(k, st.a) : binom(st.s, st.a)) : 1;
+        if (st.comb == COMB_GENERAL)
+            st.nterms = anch ? (st.top ? binom(k - 1, st.a - 1) : binom(st.s - 1, st.a - 1))
+                             : (st.top ? binom(k, st.a) : binom(st.s, st.a));
+        else
+            st.nterms = 1;
         st.ema_terms = (st.comb == COMB_GENERAL) ? (double)n * (double)st.cs * (double)st.nterms : 0.0;
         st.alg_bytes = bytes;
-        st.gt = pick_gt(std::max({st.ldp, st.lds, st.comb == COMB_GENERAL ? st.lda : 0}), vn);
+        st.gt = pick_gt(std::max({st.ldp, st.ldb, st.lds, st.comb == COMB_GENERAL ? st.lda : 0}), vn);
         model += mbytes / kHbm + st.ema_terms / kTermRate;
         alg_total += bytes;
         pl.steps.push_back(st);
     }
     pl.tables_bytes = round_up(arena, 256);
     pl.ldh = round_up(k, vn);
+    pl.kp = round_up(k, 4);
     pl.hist_bytes = pl.need_hist ? n * pl.ldh * pl.elem : 0;
     if (pl.need_hist) {
         double hb = nnz * 4.0 + nnz * 1.0 + n * 12.0 + n * (double)k * E;
         model += (nnz * 4.0 + nnz * 32.0 + pl.hist_bytes) / kHbm;
         alg_total += hb;
+    }
+    if (anch) {  // colour counts + colour-bucketed CSR, once per colouring
+        double bb = 2.0 * nnz * 4.0 + nnz * 4.0 + n * 16.0 + n * (double)pl.kp * 4.0;
+        model += (bb + nnz * 32.0) / kHbm;
+        alg_total += bb;
     }
     pl.model_time = model;
     pl.alg_bytes_total = alg_total;
@@ -337,6 +368,8 @@ static bool plan_chain(const Template &t, const Chain &c, int root, int64_t n, i
     int64_t off = pl.tables_bytes;
     pl.off_colors = off;  off = round_up(off + std::max<int64_t>(n, 1) + 16, 256);
     pl.off_hist = off;    off = round_up(off + pl.hist_bytes, 256);
+    pl.off_hcnt = off;    off = round_up(off + (anch ? n * pl.kp * 4 : 0), 256);
+    pl.off_bcol = off;    off = round_up(off + (anch ? nnz * 4 : 0), 256);
     pl.off_rowval = off;  off = round_up(off + std::max<int64_t>(n, 1) * 8, 256);
     pl.off_partial = off; off = round_up(off + kReduceBlocks * 8, 256);
     pl.off_results = off; off = round_up(off + kResultsRing * 8, 256);
@@ -347,46 +380,90 @@ static bool plan_chain(const Template &t, const Chain &c, int root, int64_t n, i
 static bool build_index(Plan &pl) {
     const int k = pl.k;
     const uint32_t full = (k == 32) ? 0xffffffffu : ((1u << k) - 1);
+    const bool anch = pl.layout == LAYOUT_ANCHORED;
+    const int K = anch ? k - 1 : k;                 // universe of the stored colour sets
+    const uint32_t fullK = (K >= 32) ? 0xffffffffu : ((1u << K) - 1);
     pl.index.clear();
+    auto align = [&]() { while (pl.index.size() % 4) pl.index.push_back(0); };
+    std::map<int, int64_t> push_maps;               // anchored push map per passive size p
     for (Step &st : pl.steps) {
-        while (pl.index.size() % 4) pl.index.push_back(0);   // 16-B aligned tables (int2 loads)
+        // ---- anchored gather: push map [x][ci][u] -> B column (or -1) ----
+        if (anch && st.src == SRC_GATHER && !(st.top && st.comb == COMB_ACTIVE_LEAF)) {
+            auto it = push_maps.find(st.p);
+            if (it != push_maps.end()) {
+                st.map_off = it->second;
+            } else {
+                double need = (double)k * k * (double)st.cp;
+                if (need > 1.5e9) { set_error("push map too large"); return false; }
+                align();
+                st.map_off = (int64_t)pl.index.size();
+                std::vector<uint32_t> us;
+                for_each_subset(k - 1, st.p - 1, [&](uint32_t m) { us.push_back(m); });
+                for (int x = 0; x < k; ++x)
+                    for (int ci = 0; ci < k; ++ci)
+                        for (uint32_t u : us) {
+                            int32_t tcol = -1;
+                            if (x != ci) {
+                                uint32_t U = insert_gap(u, x);            // subset of [k] \ {x}
+                                if (!(U >> ci & 1u))
+                                    tcol = (int32_t)colex_rank(drop_bit(U | (1u << x), ci));
+                            }
+                            pl.index.push_back(tcol);
+                        }
+                push_maps[st.p] = st.map_off;
+            }
+        }
+        align();
         st.idx_off = (int64_t)pl.index.size();
         if (st.top && st.comb == COMB_ACTIVE_LEAF) {
-            // colorful_i = B(i, [k] \ {c(i)}): column per colour x
-            for (int x = 0; x < k; ++x) pl.index.push_back((int32_t)colex_rank(full ^ (1u << x)));
+            if (!anch) {
+                // colorful_i = B(i, [k] \ {c(i)}): column per colour x
+                for (int x = 0; x < k; ++x) pl.index.push_back((int32_t)colex_rank(full ^ (1u << x)));
+            } else {
+                // colorful_i = Σ_{x≠c(i)} Σ_{j: c(j)=x} M_p(j, [k]\{x,c(i)} relabelled wrt x): [x][ci]
+                for (int x = 0; x < k; ++x)
+                    for (int ci = 0; ci < k; ++ci)
+                        pl.index.push_back(x == ci ? -1
+                                                   : (int32_t)colex_rank(drop_bit(full & ~(1u << x) & ~(1u << ci), x)));
+            }
             pl.top_leaf_col_off = (int)st.idx_off;
         } else if (st.comb == COMB_ACTIVE_LEAF) {
-            // M_s(i,S) = [c(i) ∈ S]·B(i, S \ {c(i)}): map[x][o]
-            double need = (double)k * (double)st.cs;
-            if (need > 1.5e9) { set_error("index table too large"); return false; }
-            std::vector<uint32_t> outs;
-            outs.reserve(st.cs);
-            for_each_subset(k, st.s, [&](uint32_t m) { outs.push_back(m); });
-            for (int x = 0; x < k; ++x)
-                for (uint32_t S : outs)
-                    pl.index.push_back((S >> x & 1u) ? (int32_t)colex_rank(S ^ (1u << x)) : -1);
+            if (!anch) {
+                // M_s(i,S) = [c(i) ∈ S]·B(i, S \ {c(i)}): map[x][o]
+                double need = (double)k * (double)st.cs;
+                if (need > 1.5e9) { set_error("index table too large"); return false; }
+                std::vector<uint32_t> outs;
+                outs.reserve(st.cs);
+                for_each_subset(k, st.s, [&](uint32_t m) { outs.push_back(m); });
+                for (int x = 0; x < k; ++x)
+                    for (uint32_t S : outs)
+                        pl.index.push_back((S >> x & 1u) ? (int32_t)colex_rank(S ^ (1u << x)) : -1);
+            }
+            // anchored leaf-active: M_s(i,·) = B(i,·), no table
         } else {
-            // GENERAL: (I_a, I_p) for every split of every output colour set
+            // GENERAL: (I_a, I_p) for every split of every output colour set;
+            // anchored: universe [k-1], sizes (s-1, a-1, p) — one table for every vertex
             double need = 2.0 * (double)st.cs * (double)st.nterms;
             if (need > 1.5e9) { set_error("split table too large"); return false; }
+            const int asz = anch ? st.a - 1 : st.a;
             auto emit = [&](uint32_t S) {
                 for (uint32_t sub = S;; sub = (sub - 1) & S) {
-                    if (__builtin_popcount(sub) == st.a) {
+                    if (__builtin_popcount(sub) == asz) {
                         pl.index.push_back((int32_t)colex_rank(sub));
                         pl.index.push_back((int32_t)colex_rank(S ^ sub));
                     }
                     if (sub == 0) break;
                 }
             };
-            if (st.top) emit(full);
-            else for_each_subset(k, st.s, emit);
+            if (st.top) emit(fullK);
+            else for_each_subset(K, anch ? st.s - 1 : st.s, emit);
         }
     }
     if (pl.index.empty()) pl.index.push_back(0);
     return true;
 }
 
-sg2v_status make_plan(const Template &t, int64_t n, int64_t nnz, sg2v_precision prec,
+sg2v_status make_plan(const Template &t, int64_t n, int64_t nnz, sg2v_precision prec, Layout layout,
                       std::unique_ptr<Plan> &out) {
     std::unique_ptr<Plan> best;
     int r0 = 0, r1 = t.k - 1;
@@ -395,7 +472,7 @@ sg2v_status make_plan(const Template &t, int64_t n, int64_t nnz, sg2v_precision 
         for (int policy = 0; policy < 3; ++policy) {
             Chain c = build_chain(t, root, policy);
             auto pl = std::make_unique<Plan>();
-            plan_chain(t, c, root, n, nnz, prec, *pl);
+            plan_chain(t, c, root, n, nnz, prec, layout, *pl);
             bool better = !best || pl->model_time < best->model_time * (1 - 1e-9) ||
                           (pl->model_time <= best->model_time * (1 + 1e-9) && pl->ws_bytes < best->ws_bytes);
             if (better) best = std::move(pl);
@@ -409,6 +486,7 @@ sg2v_status make_plan(const Template &t, int64_t n, int64_t nnz, sg2v_precision 
 std::string Plan::describe() const {
     std::ostringstream o;
     o << "{\"k\":" << k << ",\"root\":" << root << ",\"elem\":" << elem
+      << ",\"layout\":\"" << (layout == LAYOUT_ANCHORED ? "anchored" : "dense") << "\""
       << ",\"precision\":\"" << (prec == SG2V_F32 ? "f32" : prec == SG2V_F64 ? "f64" : "u64") << "\""
       << ",\"need_hist\":" << (need_hist ? "true" : "false") << ",\"hist_bytes\":" << hist_bytes
       << ",\"tables_bytes\":" << tables_bytes << ",\"workspace_bytes\":" << ws_bytes
@@ -420,7 +498,7 @@ std::string Plan::describe() const {
           << ",\"src\":\"" << (s.src == SRC_GATHER ? "gather" : "hist") << "\""
           << ",\"comb\":\"" << (s.comb == COMB_ACTIVE_LEAF ? "active_leaf" : "general") << "\""
           << ",\"cs\":" << s.cs << ",\"ca\":" << s.ca << ",\"cp\":" << s.cp
-          << ",\"lds\":" << s.lds << ",\"ldp\":" << s.ldp << ",\"nterms\":" << s.nterms
+          << ",\"cb\":" << s.cb << ",\"lds\":" << s.lds << ",\"ldp\":" << s.ldp << ",\"nterms\":" << s.nterms
           << ",\"gt\":" << s.gt << ",\"alg_bytes\":" << s.alg_bytes << ",\"ema_terms\":" << s.ema_terms << "}";
     }
     o << "]}";

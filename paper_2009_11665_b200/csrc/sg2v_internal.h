@@ -46,8 +46,11 @@ struct Step {
     bool top = false;
     StepSrc src = SRC_GATHER;
     StepComb comb = COMB_ACTIVE_LEAF;
-    int64_t cs = 0, ca = 0, cp = 0;        // dense column counts C(k,·)
-    int64_t lds = 0, lda = 0, ldp = 0;     // padded row strides (elements)
+    int64_t cs = 0, ca = 0, cp = 0;        // row widths of M_s, M_a, M_p (dense: C(k,·);
+                                           //   anchored: C(k-1,·-1))
+    int64_t cb = 0;                        // width of B(i,·) (dense: = cp; anchored: C(k-1,p))
+    int64_t lds = 0, lda = 0, ldp = 0, ldb = 0;  // padded row strides (elements)
+    int64_t map_off = -1;                  // anchored gather: push map [x][c(i)][u] (int32 offset)
     int buf_out = -1, buf_a = -1, buf_p = -1;  // workspace buffers (-1: none / leaf / H)
     int64_t idx_off = 0;                   // int32 offset into the plan's index blob
     int64_t nterms = 0;                    // splits per output (GENERAL)
@@ -60,8 +63,11 @@ struct Buffer {
     int64_t offset = 0, bytes = 0;
 };
 
+enum Layout { LAYOUT_ANCHORED = 0, LAYOUT_DENSE = 1 };
+
 struct Plan {
     int k = 0, root = 0;
+    Layout layout = LAYOUT_ANCHORED;
     int elem = 4;                 // sizeof element
     sg2v_precision prec = SG2V_F32;
     std::vector<Node> nodes;
@@ -70,7 +76,9 @@ struct Plan {
     int64_t ldh = 0;              // histogram row stride (elements)
     std::vector<Buffer> bufs;     // count tables (offsets inside the workspace)
     int64_t tables_bytes = 0;     // peak of the table arena
+    int64_t kp = 0;               // anchored: hcnt row stride (int32 colour counts)
     int64_t off_colors = 0, off_hist = 0, off_rowval = 0, off_partial = 0, off_results = 0;
+    int64_t off_hcnt = 0, off_bcol = 0;   // anchored: colour counts + colour-bucketed CSR
     int64_t ws_bytes = 0;
     std::vector<int32_t> index;   // concatenated index tables (host copy)
     int32_t *d_index = nullptr;   // device copy (owned by the template's cache)
@@ -94,14 +102,14 @@ struct Template {
     std::vector<std::vector<int>> adj;
     double alpha = 1.0;
     double P = 1.0;
-    std::map<std::tuple<int, int64_t, int64_t, int>, std::unique_ptr<Plan>> plans;
+    std::map<std::tuple<int, int64_t, int64_t, int, int>, std::unique_ptr<Plan>> plans;
     ~Template();
 };
 
 // planner.cpp
 sg2v_status validate_template(int k, const int32_t *edges, Template &t);
 double automorphisms(const Template &t);
-sg2v_status make_plan(const Template &t, int64_t n, int64_t nnz, sg2v_precision prec,
+sg2v_status make_plan(const Template &t, int64_t n, int64_t nnz, sg2v_precision prec, Layout layout,
                       std::unique_ptr<Plan> &out);
 int64_t binom(int n, int r);
 
@@ -109,6 +117,10 @@ int64_t binom(int n, int r);
 struct Profiler;
 int launch_colorize(uint64_t seed, int64_t j, int64_t n, int k, uint8_t *out, void *stream);
 int launch_hist(const Graph &g, const Plan &pl, const uint8_t *colors, void *H, void *stream);
+int launch_bucket(const Graph &g, const Plan &pl, const uint8_t *colors, int32_t *hcnt, int32_t *bcol,
+                  void *stream);
+int launch_astep(const Graph &g, const Plan &pl, const Step &st, const uint8_t *colors, const int32_t *hcnt,
+                 const int32_t *bcol, char *tables, void *rowval, void *stream);
 int launch_step(const Graph &g, const Plan &pl, const Step &st, const uint8_t *colors,
                 const void *H, char *tables, void *rowval, void *stream);
 int launch_reduce(const Plan &pl, int64_t n, const void *rowval, void *partial, void *result,

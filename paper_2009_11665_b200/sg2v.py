@@ -45,6 +45,7 @@ class Options(ctypes.Structure):
         ("workspace", ctypes.c_void_p),
         ("workspace_bytes", ctypes.c_uint64),
         ("row_values", ctypes.c_void_p),
+        ("layout", ctypes.c_int32),
     ]
 
 
@@ -202,13 +203,26 @@ def template_build(k, edges, root_hint=-1) -> Template:
     return Template(h, int(k), list(edges))
 
 
-def workspace_bytes(graph: Graph, tmpl: Template, precision="f32") -> int:
+LAYOUTS = {"anchored": 0, "dense": 1}
+
+
+def _set_layout(layout):
+    """Thread-local options carry the layout used by the planning queries."""
+    o = Options()
+    lib().sg2v_options_default(ctypes.byref(o))
+    o.layout = LAYOUTS[layout]
+    _check(lib().sg2v_set_options(ctypes.byref(o)))
+
+
+def workspace_bytes(graph: Graph, tmpl: Template, precision="f32", layout="anchored") -> int:
+    _set_layout(layout)
     b = ctypes.c_uint64()
     _check(lib().sg2v_workspace_bytes(graph.handle, tmpl.handle, PRECISIONS[precision], ctypes.byref(b)))
     return int(b.value)
 
 
-def plan_describe(graph: Graph, tmpl: Template, precision="f32") -> dict:
+def plan_describe(graph: Graph, tmpl: Template, precision="f32", layout="anchored") -> dict:
+    _set_layout(layout)
     need = ctypes.c_uint64()
     _check(lib().sg2v_plan_describe(graph.handle, tmpl.handle, PRECISIONS[precision], None, 0, ctypes.byref(need)))
     buf = ctypes.create_string_buffer(int(need.value))
@@ -217,8 +231,9 @@ def plan_describe(graph: Graph, tmpl: Template, precision="f32") -> dict:
     return json.loads(buf.value.decode())
 
 
-def plan_describe_n(n: int, nnz: int, tmpl: Template, precision="f32") -> dict:
+def plan_describe_n(n: int, nnz: int, tmpl: Template, precision="f32", layout="anchored") -> dict:
     """Host-only planning (no graph handle, no GPU)."""
+    _set_layout(layout)
     need = ctypes.c_uint64()
     _check(lib().sg2v_plan_describe_n(int(n), int(nnz), tmpl.handle, PRECISIONS[precision], None, 0,
                                       ctypes.byref(need)))
@@ -244,12 +259,14 @@ class Workspace:
 
 def count(graph: Graph, tmpl: Template, n_iter: int, seed: int, precision="f32", iter_offset=0,
           iter_stride=1, workspace: Workspace | None = None, stream=None, row_values=None,
-          allow_overflow=False, mem_budget_bytes=0):
+          allow_overflow=False, mem_budget_bytes=0, layout="anchored"):
     """sg2v_count_ex.  Returns (estimate, colorful) — colorful is float64[n_iter]
     (F32/F64) or uint64[n_iter] (U64, residues mod 2^64).  row_values: optional
     CUDA tensor (float64 or int64/uint64, n entries) receiving the per-vertex
-    values of the last colouring."""
+    values of the last colouring.  layout: "anchored" (default) or "dense"."""
     prec = PRECISIONS[precision]
+    if workspace is None and graph.n > 0 and tmpl.k > 1:
+        workspace = Workspace(workspace_bytes(graph, tmpl, precision, layout))
     o = Options()
     lib().sg2v_options_default(ctypes.byref(o))
     o.precision = prec
@@ -257,8 +274,7 @@ def count(graph: Graph, tmpl: Template, n_iter: int, seed: int, precision="f32",
     o.iter_stride = int(iter_stride)
     o.stream = stream if stream is not None else _cur_stream()
     o.mem_budget_bytes = int(mem_budget_bytes)
-    if workspace is None and graph.n > 0 and tmpl.k > 1:
-        workspace = Workspace(workspace_bytes(graph, tmpl, precision))
+    o.layout = LAYOUTS[layout]
     if workspace is not None:
         o.workspace = workspace.ptr
         o.workspace_bytes = workspace.nbytes

@@ -72,8 +72,9 @@ def test_plan_invariants(name):
     k = 1 + max(max(x) for x in e)
     T = sg.template_build(k, e)
     for prec in ("f32", "f64", "u64"):
-        d = sg.plan_describe_n(1 << 20, 200 << 20, T, prec)
+        d = sg.plan_describe_n(1 << 20, 200 << 20, T, prec, "dense")
         steps = d["steps"]
+        assert d["layout"] == "dense"
         assert len(steps) == k - 1                      # k-1 splits (2k-1 nodes)
         assert steps[-1]["top"] and steps[-1]["s"] == k
         elem = 4 if prec == "f32" else 8
@@ -82,11 +83,24 @@ def test_plan_invariants(name):
             assert s["cp"] == math.comb(k, s["p"])         # C(k,|T_p|) traversals
             assert s["ca"] == math.comb(k, s["a"])
             if not s["top"]:
-                assert s["cs"] == math.comb(k, s["s"])
+                assert s["cs"] == math.comb(k, s["s"])     # n x C(k,|T_s|) tables
                 assert s["lds"] * elem % 16 == 0
             if s["comb"] == "general":
                 assert s["nterms"] == (math.comb(k, s["a"]) if s["top"] else math.comb(s["s"], s["a"]))
         assert d["workspace_bytes"] >= d["tables_bytes"] > 0 or k <= 2
+        # root-colour anchored layout: only colour sets containing c(i) are stored
+        a = sg.plan_describe_n(1 << 20, 200 << 20, T, prec, "anchored")
+        assert a["layout"] == "anchored" and len(a["steps"]) == k - 1
+        for s in a["steps"]:
+            assert s["s"] == s["a"] + s["p"]
+            assert s["cp"] == math.comb(k - 1, s["p"] - 1)
+            assert s["cb"] == math.comb(k - 1, s["p"])
+            if not s["top"]:
+                assert s["cs"] == math.comb(k - 1, s["s"] - 1)
+            if s["comb"] == "general":
+                assert s["nterms"] == (math.comb(k - 1, s["a"] - 1) if s["top"] else math.comb(s["s"] - 1, s["a"] - 1))
+        if k >= 4:
+            assert a["tables_bytes"] < d["tables_bytes"]
 
 
 def test_root_hint_changes_plan_not_sizes():

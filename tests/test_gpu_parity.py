@@ -34,35 +34,39 @@ def _load(g):
     return sg.graph_load_csr(g.n, g.row_offsets, g.col_indices, validate=True)
 
 
-def _rows(G, T, seed, j, prec):
+LAYOUTS = ("anchored", "dense")
+
+
+def _rows(G, T, seed, j, prec, layout="anchored"):
     dt = torch.int64 if prec == "u64" else torch.float64
     rv = torch.zeros(max(G.n, 1), dtype=dt, device="cuda")
     _, tot = sg.count(G, T, n_iter=1, seed=seed, iter_offset=j, precision=prec, row_values=rv,
-                      allow_overflow=True)
+                      allow_overflow=True, layout=layout)
     r = rv.cpu().numpy()[:G.n]
     return tot[0], (r.view(np.uint64) if prec == "u64" else r)
 
 
-def _check_all(oracle, g, e, seeds_js, roots=(-1,), precs=("u64", "f64", "f32"), rows=True):
+def _check_all(oracle, g, e, seeds_js, roots=(-1,), precs=("u64", "f64", "f32"), rows=True, layouts=LAYOUTS):
     k = _k(e)
     G = _load(g)
     for root in roots:
         T = sg.template_build(k, e, root_hint=root)
         for seed, j in seeds_js:
             cols = oracle.colors(seed, j, g.n, k)
-            for prec in precs:
+            for prec, layout in [(p, l) for p in precs for l in layouts]:
                 # per-vertex values count embeddings with the ROOT mapped to i, so the
                 # oracle is rooted where the planner rooted (the total is root-free)
-                rho = sg.plan_describe(G, T, prec).get("root", 0) if k > 1 else 0
+                rho = sg.plan_describe(G, T, prec, layout).get("root", 0) if k > 1 else 0
                 want_u, want_ru = oracle.count(g, k, e, cols, root=rho, rows=True)
                 want_f, vmax, want_rf = oracle.count(g, k, e, cols, root=rho, arith=oracle.ARITH_F64, rows=True)
                 if rows:
-                    tot, r = _rows(G, T, seed, j, prec)
+                    tot, r = _rows(G, T, seed, j, prec, layout)
                 else:
-                    _, t = sg.count(G, T, n_iter=1, seed=seed, iter_offset=j, precision=prec, allow_overflow=True)
+                    _, t = sg.count(G, T, n_iter=1, seed=seed, iter_offset=j, precision=prec, allow_overflow=True,
+                                    layout=layout)
                     tot, r = t[0], None
                 if prec == "u64":
-                    assert int(tot) == want_u, (root, seed, j)
+                    assert int(tot) == want_u, (root, seed, j, layout)
                     if r is not None:
                         assert np.array_equal(r, want_ru)
                 elif prec == "f64":
@@ -101,8 +105,8 @@ def test_d1_u3_er1000_100_colourings(oracle):
     G = _load(g)
     T = sg.template_build(3, e)
     want = [oracle.count(g, 3, e, oracle.colors(1, j, g.n, 3)) for j in range(100)]
-    for prec in ("u64", "f64", "f32"):
-        est, got = sg.count(G, T, n_iter=100, seed=1, precision=prec)
+    for prec, layout in [(p, l) for p in ("u64", "f64", "f32") for l in LAYOUTS]:
+        est, got = sg.count(G, T, n_iter=100, seed=1, precision=prec, layout=layout)
         assert [int(x) for x in got] == want  # all values < 2^24: bit-exact in every mode
         if prec != "u64":
             P = math.factorial(3) / 27
