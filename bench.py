@@ -43,6 +43,7 @@ def _args():
     p.add_argument("--impl", default="sg2v", choices=["sg2v", "reference"])
     p.add_argument("--template", default="u15-1")
     p.add_argument("--precision", default="f32", choices=["f32", "f64", "u64"])
+    p.add_argument("--layout", default="anchored", choices=["anchored", "dense"])
     p.add_argument("--scale", type=int, default=20)
     p.add_argument("--seed", type=int, default=1)
     p.add_argument("--no-cpu-baseline", action="store_true")
@@ -213,7 +214,7 @@ def run_sg2v(args):
 
     G = sg.graph_load_csr(g.n, g.row_offsets, g.col_indices)
     T = sg.template_build(k, edges)
-    plan = sg.plan_describe(G, T, args.precision)
+    plan = sg.plan_describe(G, T, args.precision, args.layout)
     ws = sg.Workspace(plan["workspace_bytes"])
 
     def colouring(t):  # colouring index of this rank's t-th colouring
@@ -222,7 +223,7 @@ def run_sg2v(args):
     # warm-up (untimed)
     for t in range(args.warmup):
         sg.count(G, T, n_iter=1, seed=args.seed, iter_offset=colouring(t), precision=args.precision,
-                 workspace=ws, allow_overflow=True)
+                 workspace=ws, allow_overflow=True, layout=args.layout)
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
@@ -235,7 +236,7 @@ def run_sg2v(args):
         torch.cuda.synchronize()
         ev0.record(stream)
         est, c = sg.count(G, T, n_iter=args.steps, seed=args.seed, iter_offset=colouring(args.warmup),
-                          iter_stride=world, precision=args.precision, workspace=ws, allow_overflow=True)
+                          iter_stride=world, precision=args.precision, workspace=ws, allow_overflow=True, layout=args.layout)
         for t in range(args.steps):
             counts[rank + world * t] = float(c[t])
         if world > 1:
@@ -262,7 +263,7 @@ def run_sg2v(args):
     for t in range(e2e_steps):
         Ge = sg.graph_load_csr(g.n, ro_h.numpy(), ci_h.numpy())
         sg.count(Ge, T, n_iter=1, seed=args.seed, iter_offset=colouring(args.warmup + args.steps + t),
-                 precision=args.precision, workspace=ws, allow_overflow=True)  # includes D2H of the count
+                 precision=args.precision, workspace=ws, allow_overflow=True, layout=args.layout)  # includes D2H of the count
         Ge.free()
     e1.record(stream)
     torch.cuda.synchronize()
@@ -291,7 +292,7 @@ def run_sg2v(args):
     if os.path.exists(tr_path):
         try:
             tr = json.load(open(tr_path))
-            key = f"{args.template}/{args.precision}/scale{args.scale}"
+            key = f"{args.template}/{args.precision}/{args.layout}/scale{args.scale}"
             if key in tr:
                 traffic = tr[key]
         except Exception:
@@ -305,7 +306,8 @@ def run_sg2v(args):
         "warmup": args.warmup, "ms_per_step": value * 1e3, "higher_is_better": False, "scaling": "weak",
         "vs_baseline": None, "dtype": args.precision, "data": "synthetic",
         "config": {"workload": _workload_name(args, g), "template": args.template, "k": k,
-                   "precision": args.precision, "graph": stats, "parallelism": f"replicas{world}",
+                   "precision": args.precision, "layout": args.layout, "graph": stats,
+                   "parallelism": f"replicas{world}",
                    "colourings": total, "root": plan["root"], "workspace_GB": plan["workspace_bytes"] / 1e9,
                    "l2": "inputs larger than L2 (CSR %.2f GB + count tables %.1f GB >> 126 MB); no flush"
                          % (g.nbytes() / 1e9, plan["tables_bytes"] / 1e9)},
