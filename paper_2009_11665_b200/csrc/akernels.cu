@@ -18,6 +18,8 @@
 //  atop_leaf_kernel  top step with a leaf active child: one column per edge
 #include <cuda_runtime.h>
 
+#include <cstdlib>
+
 #include "kcommon.cuh"
 #include "sg2v_internal.h"
 
@@ -100,12 +102,11 @@ struct AStepArgs {
     int64_t smem_group;
 };
 
-template <typename T, typename RT, int GT>
+// GT threads per row group; R 16-B vectors per thread per pass; U neighbours in flight
+template <typename T, typename RT, int GT, int R, int U>
 __global__ void __launch_bounds__(256) astep_kernel(AStepArgs A) {
     constexpr int G = 256 / GT;
     constexpr int VN = Vec<T>::N;
-    constexpr int R = 4;
-    constexpr int U = 4;
     extern __shared__ __align__(16) unsigned char smem[];
     __shared__ RT red[8];
     const int g = threadIdx.x / GT, t = threadIdx.x % GT;
@@ -280,9 +281,9 @@ int launch_bucket(const Graph &g, const Plan &pl, const uint8_t *colors, int32_t
     return (int)cudaGetLastError();
 }
 
-template <typename T, typename RT, int GT>
+template <typename T, typename RT, int GT, int R, int U>
 static int launch_astep_t(const AStepArgs &A, void *stream) {
-    auto kern = astep_kernel<T, RT, GT>;
+    auto kern = astep_kernel<T, RT, GT, R, U>;
     constexpr int G = 256 / GT;
     size_t smem = (size_t)G * A.smem_group * sizeof(T);
     if (smem > 227 * 1024) return -1;
@@ -302,17 +303,43 @@ static int launch_astep_t(const AStepArgs &A, void *stream) {
     return (int)cudaGetLastError();
 }
 
-template <typename T, typename RT>
+// Row-group configuration: narrow rows give every vector of the passive row its own
+// lane (R = 1) and keep U = 8 neighbours in flight; rows wider than 256 vectors use
+// the whole CTA, one vector per lane per pass with U = 16 neighbours in flight
+// (measured best of R/U in {1/16, 2/8, 4/4} on u15-1, RMAT-1M-like).
+template <typename T, typename RT, int R, int U>
 static int launch_astep_gt(const AStepArgs &A, int gt, void *stream) {
     switch (gt) {
-        case 4: return launch_astep_t<T, RT, 4>(A, stream);
-        case 8: return launch_astep_t<T, RT, 8>(A, stream);
-        case 16: return launch_astep_t<T, RT, 16>(A, stream);
-        case 32: return launch_astep_t<T, RT, 32>(A, stream);
-        case 64: return launch_astep_t<T, RT, 64>(A, stream);
-        case 128: return launch_astep_t<T, RT, 128>(A, stream);
-        default: return launch_astep_t<T, RT, 256>(A, stream);
+        case 4: return launch_astep_t<T, RT, 4, R, U>(A, stream);
+        case 8: return launch_astep_t<T, RT, 8, R, U>(A, stream);
+        case 16: return launch_astep_t<T, RT, 16, R, U>(A, stream);
+        case 32: return launch_astep_t<T, RT, 32, R, U>(A, stream);
+        case 64: return launch_astep_t<T, RT, 64, R, U>(A, stream);
+        case 128: return launch_astep_t<T, RT, 128, R, U>(A, stream);
+        default: return launch_astep_t<T, RT, 256, R, U>(A, stream);
     }
+}
+
+template <typename T, typename RT>
+static int launch_astep_cfg(const AStepArgs &A, void *stream) {
+    constexpr int VN = Vec<T>::N;
+    static int tune = -1;  // SG2V_TUNE (experiments only): 1 narrow U=16; 2 wide R=2/U=8; 4 wide R=4/U=4
+    if (tune < 0) {
+        const char *e = getenv("SG2V_TUNE");
+        tune = e ? atoi(e) : 0;
+    }
+    const int64_t nvec = A.src_hist ? 1 : A.ldp / VN;
+    const int64_t nout = std::max(A.ldb, A.lds) / VN;
+    int64_t want = std::max<int64_t>(nvec, (nout + 3) / 4);
+    int gt = 4;
+    while (gt < want && gt < 256) gt *= 2;
+    if (nvec > 256) {
+        if (tune == 2) return launch_astep_t<T, RT, 256, 2, 8>(A, stream);
+        if (tune == 4) return launch_astep_t<T, RT, 256, 4, 4>(A, stream);
+        return launch_astep_t<T, RT, 256, 1, 16>(A, stream);
+    }
+    if (tune == 1) return launch_astep_gt<T, RT, 1, 16>(A, gt, stream);
+    return launch_astep_gt<T, RT, 1, 8>(A, gt, stream);
 }
 
 int launch_astep(const Graph &g, const Plan &pl, const Step &st, const uint8_t *colors, const int32_t *hcnt,
@@ -369,9 +396,9 @@ int launch_astep(const Graph &g, const Plan &pl, const Step &st, const uint8_t *
     int cls = st.top ? 3 : 2;
     prof_begin(cls, stream);
     int rc;
-    if (pl.prec == SG2V_F32) rc = launch_astep_gt<float, double>(A, st.gt, stream);
-    else if (pl.prec == SG2V_F64) rc = launch_astep_gt<double, double>(A, st.gt, stream);
-    else rc = launch_astep_gt<u64, u64>(A, st.gt, stream);
+    if (pl.prec == SG2V_F32) rc = launch_astep_cfg<float, double>(A, stream);
+    else if (pl.prec == SG2V_F64) rc = launch_astep_cfg<double, double>(A, stream);
+    else rc = launch_astep_cfg<u64, u64>(A, stream);
     prof_end(cls, st.alg_bytes, stream);
     return rc;
 }

@@ -214,15 +214,21 @@ def test_errors():
 
 
 def test_determinism_and_sharding():
+    # bitwise determinism (fixed summation order, no atomics); promised for U64 and F64
+    # below 2^53; F32 is also run-to-run identical in this build
     g = rmat(12, 60_000, 0.45, 0.22, 0.22, seed=5)
     G = _load(g)
     T = sg.template_build(7, TEMPLATES["u7-2"])
-    _, a = sg.count(G, T, n_iter=8, seed=11, precision="f32")
-    _, b = sg.count(G, T, n_iter=8, seed=11, precision="f32")
-    assert np.array_equal(a, b)                                   # run-to-run bitwise
-    _, s0 = sg.count(G, T, n_iter=4, seed=11, iter_offset=0, iter_stride=2, precision="f32")
-    _, s1 = sg.count(G, T, n_iter=4, seed=11, iter_offset=1, iter_stride=2, precision="f32")
-    assert np.array_equal(a[0::2], s0) and np.array_equal(a[1::2], s1)  # replica shards
+    for layout in LAYOUTS:
+        _, a = sg.count(G, T, n_iter=8, seed=11, precision="u64", layout=layout)
+        _, b = sg.count(G, T, n_iter=8, seed=11, precision="u64", layout=layout)
+        assert np.array_equal(a, b)                                   # run-to-run bitwise
+        _, s0 = sg.count(G, T, n_iter=4, seed=11, iter_offset=0, iter_stride=2, precision="u64", layout=layout)
+        _, s1 = sg.count(G, T, n_iter=4, seed=11, iter_offset=1, iter_stride=2, precision="u64", layout=layout)
+        assert np.array_equal(a[0::2], s0) and np.array_equal(a[1::2], s1)  # replica shards
+        _, f = sg.count(G, T, n_iter=8, seed=11, precision="f32", layout=layout)
+        _, f2 = sg.count(G, T, n_iter=8, seed=11, precision="f32", layout=layout)
+        assert np.array_equal(f, f2)
 
 
 def test_closed_form_tree_on_complete_graph(oracle):
