@@ -34,10 +34,16 @@ __device__ __forceinline__ unsigned lanemask_lt() {
 // ---------------------------------------------------------------------------
 // colour counts + colour-bucketed CSR (stable within each colour)
 // ---------------------------------------------------------------------------
+// bcol entries carry the neighbour's degree-rank class in bits 26..30 when
+// n < 2^26 (the L2 residency hint of the gather; kClassShift), else bare ids.
+static constexpr int kClassShift = 26;
+
 __global__ void __launch_bounds__(256) bucket_kernel(int64_t n, int k, int kp, const int64_t *__restrict__ rowptr,
                                                      const int32_t *__restrict__ col,
                                                      const uint8_t *__restrict__ colors,
+                                                     const uint8_t *__restrict__ vclass,
                                                      int32_t *__restrict__ hcnt, int32_t *__restrict__ bcol) {
+    const bool tag = n < (int64_t(1) << kClassShift);
     const int lane = threadIdx.x & 31;
     const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
     for (int64_t i = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); i < n; i += warps) {
@@ -66,7 +72,7 @@ __global__ void __launch_bounds__(256) bucket_kernel(int64_t n, int k, int kp, c
             const int c = (e < e1) ? (int)colors[j] : 255;
             const unsigned m = __match_any_sync(0xffffffffu, c);
             const int pos = __shfl_sync(0xffffffffu, run, c & 31) + __popc(m & lanemask_lt());
-            if (e < e1) bcol[e0 + pos] = j;
+            if (e < e1) bcol[e0 + pos] = tag ? (j | ((int32_t)min((int)vclass[j], 31) << kClassShift)) : j;
             for (int x = 0; x < k; ++x) {
                 const unsigned b = __ballot_sync(0xffffffffu, c == x);
                 if (lane == x) run += __popc(b);
@@ -100,6 +106,9 @@ struct AStepArgs {
     int64_t nterms;
     void *rowval;
     int64_t smem_group;
+    int tagged;         // bcol carries rank classes
+    int hot_log2;       // neighbours with class < hot_log2 are kept in L2 (evict_last)
+    int hint;           // use the L2 policies at all
 };
 
 // GT threads per row group; R 16-B vectors per thread per pass; U neighbours in flight
@@ -116,6 +125,8 @@ __global__ void __launch_bounds__(256) astep_kernel(AStepArgs A) {
     const int64_t nvec_p = A.ldp / VN;
     const size_t row_bytes = (size_t)A.ldp * sizeof(T);
     const int k = A.k;
+    const uint64_t pol_last = policy_evict_last(), pol_first = policy_evict_first();
+    constexpr int32_t kIdMask = (1 << kClassShift) - 1;
 
     for (int64_t slot = blockIdx.x; slot < nslots; slot += gridDim.x) {
         const int64_t r = slot * G + g;
@@ -149,15 +160,20 @@ __global__ void __launch_bounds__(256) astep_kernel(AStepArgs A) {
                             const int64_t e3 = e + cnt;
                             for (; e2 + U <= e3; e2 += U) {
                                 int32_t jj[U];
+                                uint64_t pol[U];
 #pragma unroll
-                                for (int u = 0; u < U; ++u) jj[u] = __ldg(A.bcol + e2 + u);
+                                for (int u = 0; u < U; ++u) {
+                                    const int32_t b = __ldg(A.bcol + e2 + u);
+                                    jj[u] = A.tagged ? (b & kIdMask) : b;
+                                    pol[u] = (A.tagged && (b >> kClassShift) < A.hot_log2) ? pol_last : pol_first;
+                                }
                                 uint4 xv[U][R];
 #pragma unroll
                                 for (int u = 0; u < U; ++u)
 #pragma unroll
                                     for (int q = 0; q < R; ++q) {
                                         const int64_t v = v0 + q * GT + t;
-                                        xv[u][q] = (v < nvec_p) ? ldg16(A.mp + (size_t)jj[u] * row_bytes + v * 16)
+                                        xv[u][q] = (v < nvec_p) ? (A.hint ? ldg16_pol(A.mp + (size_t)jj[u] * row_bytes + v * 16, pol[u]) : ldg16(A.mp + (size_t)jj[u] * row_bytes + v * 16))
                                                                 : make_uint4(0, 0, 0, 0);
                                     }
 #pragma unroll
@@ -166,7 +182,8 @@ __global__ void __launch_bounds__(256) astep_kernel(AStepArgs A) {
                                     for (int q = 0; q < R; ++q) Vec<T>::add(acc[q], xv[u][q]);
                             }
                             for (; e2 < e3; ++e2) {
-                                const int32_t j1 = __ldg(A.bcol + e2);
+                                const int32_t b1 = __ldg(A.bcol + e2);
+                                const int32_t j1 = A.tagged ? (b1 & kIdMask) : b1;
 #pragma unroll
                                 for (int q = 0; q < R; ++q) {
                                     const int64_t v = v0 + q * GT + t;
@@ -276,7 +293,7 @@ int launch_bucket(const Graph &g, const Plan &pl, const uint8_t *colors, int32_t
     double bytes = g.nnz * 9.0 + g.nnz * 4.0 + g.n * 16.0 + (double)g.n * pl.kp * 4.0;
     prof_begin(1, stream);
     bucket_kernel<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(g.n, pl.k, (int)pl.kp, g.d_rowptr, g.d_col,
-                                                                      colors, hcnt, bcol);
+                                                                      colors, g.d_vclass, hcnt, bcol);
     prof_end(1, bytes, stream);
     return (int)cudaGetLastError();
 }
@@ -393,6 +410,24 @@ int launch_astep(const Graph &g, const Plan &pl, const Step &st, const uint8_t *
     A.nterms = st.nterms;
     A.rowval = rowval;
     A.smem_group = st.ldb + (st.comb == COMB_GENERAL ? st.lda : 0);
+    A.tagged = g.n < (int64_t(1) << kClassShift);
+    {
+        // rows of the hottest H neighbours fit in ~75 MB of the 126 MB L2
+        static int64_t l2 = 0;
+        if (!l2) {
+            int dev = 0, v = 0;
+            cudaGetDevice(&dev);
+            cudaDeviceGetAttribute(&v, cudaDevAttrL2CacheSize, dev);
+            l2 = v > 0 ? v : (126ll << 20);
+        }
+        const double H = 0.6 * (double)l2 / (double)(st.ldp * pl.elem);
+        int hl = 0;
+        while (hl < 31 && (double)(1ll << (hl + 1)) <= H) ++hl;
+        A.hot_log2 = hl;
+        static int hint = -1;  // SG2V_HINT=0 disables the L2 policy (experiments)
+        if (hint < 0) { const char *e = getenv("SG2V_HINT"); hint = e ? atoi(e) : 1; }
+        A.hint = hint;
+    }
     int cls = st.top ? 3 : 2;
     prof_begin(cls, stream);
     int rc;

@@ -181,6 +181,7 @@ sg2v_status sg2v_graph_load_csr(int64_t n, const int64_t *row_offsets, const int
     if ((e = cudaMalloc(&g->d_rowptr, (n + 1) * sizeof(int64_t))) != cudaSuccess) return fail(cuda_fail("cudaMalloc rowptr", e));
     if ((e = cudaMalloc(&g->d_col, std::max<int64_t>(nnz, 1) * sizeof(int32_t))) != cudaSuccess) return fail(cuda_fail("cudaMalloc col", e));
     if ((e = cudaMalloc(&g->d_order, std::max<int64_t>(n, 1) * sizeof(int32_t))) != cudaSuccess) return fail(cuda_fail("cudaMalloc order", e));
+    if ((e = cudaMalloc(&g->d_vclass, std::max<int64_t>(n, 1))) != cudaSuccess) return fail(cuda_fail("cudaMalloc vclass", e));
     cudaMemcpyKind kind = dev_ptrs ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
     if ((e = cudaMemcpyAsync(g->d_rowptr, row_offsets, (n + 1) * sizeof(int64_t), kind, s)) != cudaSuccess) return fail(cuda_fail("copy rowptr", e));
     if (nnz > 0 && (e = cudaMemcpyAsync(g->d_col, col_indices, nnz * sizeof(int32_t), kind, s)) != cudaSuccess) return fail(cuda_fail("copy col", e));
@@ -220,6 +221,7 @@ void sg2v_graph_free(sg2v_graph *g) {
     cudaFree(g->d_rowptr);
     cudaFree(g->d_col);
     cudaFree(g->d_order);
+    cudaFree(g->d_vclass);
     cudaSetDevice(cur);
     delete g;
 }

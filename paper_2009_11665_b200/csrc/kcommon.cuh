@@ -50,6 +50,25 @@ __device__ __forceinline__ uint4 ldg16(const void *p) {
     return r;
 }
 
+// 128-bit load with an L2 eviction-priority policy (createpolicy)
+__device__ __forceinline__ uint4 ldg16_pol(const void *p, uint64_t pol) {
+    uint4 r;
+    asm volatile("ld.global.nc.L2::cache_hint.v4.u32 {%0,%1,%2,%3}, [%4], %5;"
+                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+                 : "l"(p), "l"(pol));
+    return r;
+}
+__device__ __forceinline__ uint64_t policy_evict_last() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ uint64_t policy_evict_first() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+
 // Synchronise the GT threads of row group g (GT | 256).  Groups narrower than a
 // warp sync only their own lanes, so the call is legal inside group-uniform
 // (but warp-divergent) control flow.

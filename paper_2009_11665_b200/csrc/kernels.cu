@@ -279,6 +279,11 @@ __global__ void degree_kernel(int64_t n, const int64_t *__restrict__ rowptr, int
     }
 }
 
+__global__ void vclass_kernel(int64_t n, const int32_t *__restrict__ order, uint8_t *__restrict__ vclass) {
+    for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n; r += (int64_t)gridDim.x * blockDim.x)
+        vclass[order[r]] = (uint8_t)(63 - __clzll((unsigned long long)(r + 1)));
+}
+
 __global__ void validate_kernel(int64_t n, int64_t nnz, const int64_t *__restrict__ rowptr,
                                 const int32_t *__restrict__ col, int *__restrict__ bad) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
@@ -457,6 +462,7 @@ int graph_build_order(Graph &g, void *stream) {
     e = cudaMalloc(&tmp, tmp_bytes);
     if (e == cudaSuccess) {
         cub::DeviceRadixSort::SortPairsDescending(tmp, tmp_bytes, deg, deg_sorted, ids, g.d_order, (int)n, 0, 32, s);
+        vclass_kernel<<<(unsigned)std::min<int64_t>((n + 255) / 256, 4096), 256, 0, s>>>(n, g.d_order, g.d_vclass);
         int32_t mx = 0;
         cudaMemcpyAsync(&mx, deg_sorted, sizeof(int32_t), cudaMemcpyDeviceToHost, s);
         e = cudaStreamSynchronize(s);

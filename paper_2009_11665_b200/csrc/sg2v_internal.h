@@ -25,6 +25,7 @@ struct Graph {
     int64_t *d_rowptr = nullptr;
     int32_t *d_col = nullptr;
     int32_t *d_order = nullptr;  // rows sorted by degree, descending
+    uint8_t *d_vclass = nullptr; // floor(log2(1 + rank in degree order)) per vertex (L2 hints)
     int64_t max_deg = 0;
 };
 
