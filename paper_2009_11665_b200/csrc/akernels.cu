@@ -109,6 +109,9 @@ struct AStepArgs {
     int tagged;         // bcol carries rank classes
     int hot_log2;       // neighbours with class < hot_log2 are kept in L2 (evict_last)
     int hint;           // use the L2 policies at all
+    int packed;         // split pairs packed as ia | ip << 16 (both < 2^16)
+    int stage_a;        // M_a row staged in shared memory (else read through L1)
+    int tpo;            // lanes per output in the eMA (power of 2, <= 32)
 };
 
 // GT threads per row group; R 16-B vectors per thread per pass; U neighbours in flight
@@ -135,7 +138,7 @@ __global__ void __launch_bounds__(256) astep_kernel(AStepArgs A) {
         const int ci = act ? (int)A.colors[i] : 0;
         if (act) {
             for (int64_t v = t; v < A.ldb / VN; v += GT) reinterpret_cast<uint4 *>(sB)[v] = make_uint4(0, 0, 0, 0);
-            if (A.comb == COMB_GENERAL) {
+            if (A.comb == COMB_GENERAL && A.stage_a) {
                 const char *a = A.ma + (size_t)i * A.lda * sizeof(T);
                 for (int64_t v = t; v < A.lda / VN; v += GT) reinterpret_cast<uint4 *>(sA)[v] = ldg16(a + v * 16);
             }
@@ -223,24 +226,64 @@ __global__ void __launch_bounds__(256) astep_kernel(AStepArgs A) {
                     for (int64_t v = t; v < A.lds / VN; v += GT)
                         reinterpret_cast<uint4 *>(out)[v] = reinterpret_cast<const uint4 *>(sB)[v];
                 } else {
-                    const int2 *sp = reinterpret_cast<const int2 *>(A.idx);
-                    for (int64_t o = t; o < A.lds; o += GT) {
+                    // split table term-major: entry (w, o) at w*cs + o, so the lanes
+                    // (consecutive outputs o) read consecutive words.  With few outputs
+                    // (cs < GT) tpo consecutive lanes share an output and split its terms.
+                    const T *ga = reinterpret_cast<const T *>(A.ma) + (size_t)i * A.lda;
+                    const int tpo = A.tpo, cs = (int)A.cs, nt = (int)A.nterms, lds = (int)A.lds;
+                    const int l = t % tpo;
+                    for (int ob = 0; ob < lds; ob += GT / tpo) {
+                        const int o = ob + t / tpo;
                         T acc = 0;
-                        if (o < A.cs) {
-                            const int2 *p = sp + (size_t)o * A.nterms;
-                            for (int64_t w = 0; w < A.nterms; ++w) {
-                                const int2 q = __ldg(p + w);
-                                acc += sA[q.x] * sB[q.y];
+                        if (o < cs) {
+                            if (A.packed) {
+                                const uint32_t *p = reinterpret_cast<const uint32_t *>(A.idx) + o;
+                                if (A.stage_a) {
+#pragma unroll 4
+                                    for (int w = l; w < nt; w += tpo) {
+                                        const uint32_t q = __ldg(p + w * cs);
+                                        acc += sA[q & 0xffffu] * sB[q >> 16];
+                                    }
+                                } else {
+#pragma unroll 4
+                                    for (int w = l; w < nt; w += tpo) {
+                                        const uint32_t q = __ldg(p + w * cs);
+                                        acc += __ldg(ga + (q & 0xffffu)) * sB[q >> 16];
+                                    }
+                                }
+                            } else {
+                                const int2 *p = reinterpret_cast<const int2 *>(A.idx) + o;
+                                for (int w = l; w < nt; w += tpo) {
+                                    const int2 q = __ldg(p + (size_t)w * cs);
+                                    const T av = A.stage_a ? sA[q.x] : __ldg(ga + q.x);
+                                    acc += av * sB[q.y];
+                                }
                             }
                         }
-                        out[o] = acc;
+                        if (tpo > 1) {  // tpo <= 32 and GT >= 32: whole warps, uniform trip count
+#pragma unroll
+                            for (int off = 16; off > 0; off >>= 1)
+                                if (off < tpo) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+                        }
+                        if (l == 0 && o < lds) out[o] = acc;
                     }
                 }
             } else {
-                const int2 *sp = reinterpret_cast<const int2 *>(A.idx);
-                for (int64_t w = t; w < A.nterms; w += GT) {
-                    const int2 q = __ldg(sp + w);
-                    racc += (RT)sA[q.x] * (RT)sB[q.y];
+                const T *ga = reinterpret_cast<const T *>(A.ma) + (size_t)i * A.lda;
+                if (A.packed) {
+                    const uint32_t *sp = reinterpret_cast<const uint32_t *>(A.idx);
+                    for (int64_t w = t; w < A.nterms; w += GT) {
+                        const uint32_t q = __ldg(sp + w);
+                        const T av = A.stage_a ? sA[q & 0xffffu] : __ldg(ga + (q & 0xffffu));
+                        racc += (RT)av * (RT)sB[q >> 16];
+                    }
+                } else {
+                    const int2 *sp = reinterpret_cast<const int2 *>(A.idx);
+                    for (int64_t w = t; w < A.nterms; w += GT) {
+                        const int2 q = __ldg(sp + w);
+                        const T av = A.stage_a ? sA[q.x] : __ldg(ga + q.x);
+                        racc += (RT)av * (RT)sB[q.y];
+                    }
                 }
             }
         }
@@ -338,7 +381,8 @@ static int launch_astep_gt(const AStepArgs &A, int gt, void *stream) {
 }
 
 template <typename T, typename RT>
-static int launch_astep_cfg(const AStepArgs &A, void *stream) {
+static int launch_astep_cfg(const AStepArgs &A0, void *stream) {
+    AStepArgs A = A0;
     constexpr int VN = Vec<T>::N;
     static int tune = -1;  // SG2V_TUNE (experiments only): 1 narrow U=16; 2 wide R=2/U=8; 4 wide R=4/U=4
     if (tune < 0) {
@@ -350,6 +394,11 @@ static int launch_astep_cfg(const AStepArgs &A, void *stream) {
     int64_t want = std::max<int64_t>(nvec, (nout + 3) / 4);
     int gt = 4;
     while (gt < want && gt < 256) gt *= 2;
+    if (nvec > 256) gt = 256;
+    // eMA with few outputs: tpo lanes per output (whole warps only)
+    A.tpo = 1;
+    if (A.comb == COMB_GENERAL && !A.top && gt >= 32)
+        while (A.tpo < 32 && A.cs * A.tpo * 2 <= gt) A.tpo *= 2;
     if (nvec > 256) {
         if (tune == 2) return launch_astep_t<T, RT, 256, 2, 8>(A, stream);
         if (tune == 4) return launch_astep_t<T, RT, 256, 4, 4>(A, stream);
@@ -409,7 +458,11 @@ int launch_astep(const Graph &g, const Plan &pl, const Step &st, const uint8_t *
     A.idx = idx;
     A.nterms = st.nterms;
     A.rowval = rowval;
-    A.smem_group = st.ldb + (st.comb == COMB_GENERAL ? st.lda : 0);
+    A.packed = st.packed;
+    // stage M_a next to B only while both fit comfortably (occupancy); else L1
+    A.stage_a = (st.comb == COMB_GENERAL) && (st.ldb + st.lda) * pl.elem <= 100 * 1024;
+    A.tpo = 1;  // set per launch configuration (launch_astep_cfg)
+    A.smem_group = st.ldb + (A.stage_a ? st.lda : 0);
     A.tagged = g.n < (int64_t(1) << kClassShift);
     {
         // rows of the hottest H neighbours fit in ~75 MB of the 126 MB L2

@@ -200,7 +200,7 @@ static int pick_gt(int64_t cols, int vn) {
 
 
 static constexpr double kHbm = 6.5e12;     // B/s, MEASURED_PEAKS hbm_gbs (planning only)
-static constexpr double kTermRate = 2.0e12; // eMA terms/s (smem-bound estimate)
+static constexpr double kTermRate = 5.0e11; // eMA terms/s (measured order of the index-driven eMA)
 
 // Relabelling of colour sets for the root-colour-anchored layout:
 // a set over [k] \ {e} is stored as a set over [k-1] by closing the gap at e.
@@ -442,21 +442,47 @@ static bool build_index(Plan &pl) {
             // anchored leaf-active: M_s(i,·) = B(i,·), no table
         } else {
             // GENERAL: (I_a, I_p) for every split of every output colour set;
-            // anchored: universe [k-1], sizes (s-1, a-1, p) — one table for every vertex
+            // anchored: universe [k-1], sizes (s-1, a-1, p) — one table for every vertex,
+            // stored term-major (entry (w, o) at w*cs + o) and packed ia | ip << 16
+            // when both ranks fit 16 bits; dense: output-major int2 pairs
             double need = 2.0 * (double)st.cs * (double)st.nterms;
             if (need > 1.5e9) { set_error("split table too large"); return false; }
             const int asz = anch ? st.a - 1 : st.a;
+            std::vector<std::pair<int32_t, int32_t>> pairs;
+            pairs.reserve((size_t)(st.cs * st.nterms));
             auto emit = [&](uint32_t S) {
                 for (uint32_t sub = S;; sub = (sub - 1) & S) {
-                    if (__builtin_popcount(sub) == asz) {
-                        pl.index.push_back((int32_t)colex_rank(sub));
-                        pl.index.push_back((int32_t)colex_rank(S ^ sub));
-                    }
+                    if (__builtin_popcount(sub) == asz)
+                        pairs.push_back({(int32_t)colex_rank(sub), (int32_t)colex_rank(S ^ sub)});
                     if (sub == 0) break;
                 }
             };
             if (st.top) emit(fullK);
             else for_each_subset(K, anch ? st.s - 1 : st.s, emit);
+            if (!anch) {
+                for (auto &pq : pairs) { pl.index.push_back(pq.first); pl.index.push_back(pq.second); }
+            } else {
+                st.packed = (st.ca < 65536 && st.cb < 65536) ? 1 : 0;
+                const int64_t cs = st.cs, nt = st.nterms;
+                if (st.packed) {
+                    size_t base = pl.index.size();
+                    pl.index.resize(base + (size_t)(cs * nt));
+                    for (int64_t o = 0; o < cs; ++o)
+                        for (int64_t w = 0; w < nt; ++w) {
+                            const auto &pq = pairs[(size_t)(o * nt + w)];
+                            pl.index[base + (size_t)(w * cs + o)] = (int32_t)((uint32_t)pq.first | ((uint32_t)pq.second << 16));
+                        }
+                } else {
+                    size_t base = pl.index.size();
+                    pl.index.resize(base + (size_t)(2 * cs * nt));
+                    for (int64_t o = 0; o < cs; ++o)
+                        for (int64_t w = 0; w < nt; ++w) {
+                            const auto &pq = pairs[(size_t)(o * nt + w)];
+                            pl.index[base + 2 * (size_t)(w * cs + o)] = pq.first;
+                            pl.index[base + 2 * (size_t)(w * cs + o) + 1] = pq.second;
+                        }
+                }
+            }
         }
     }
     if (pl.index.empty()) pl.index.push_back(0);

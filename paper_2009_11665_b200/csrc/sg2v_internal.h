@@ -55,6 +55,7 @@ struct Step {
     int buf_out = -1, buf_a = -1, buf_p = -1;  // workspace buffers (-1: none / leaf / H)
     int64_t idx_off = 0;                   // int32 offset into the plan's index blob
     int64_t nterms = 0;                    // splits per output (GENERAL)
+    int packed = 0;                        // anchored GENERAL: pairs packed ia | ip << 16, term-major
     int gt = 32;                           // threads per row group (step kernel)
     double alg_bytes = 0.0;                // algorithmic HBM bytes
     double ema_terms = 0.0;

@@ -12,6 +12,9 @@ from .graphs import (  # noqa: F401
     erdos_renyi,
     rmat,
     rmat_1m_like,
+    miami_like,
+    orkut_like,
+    BIG_GRAPHS,
     cycle_graph,
     path_graph,
     complete_graph,

@@ -184,3 +184,31 @@ def degree_stats(g: CSR) -> dict:
         "p99": float(np.percentile(d, 99)) if g.n else 0.0,
         "isolated": int((d == 0).sum()),
     }
+
+
+def miami_like(seed: int = 1) -> CSR:
+    """RMAT with milder skew, scale 21, m = 5.2e7 drawn, id-permuted.
+
+    a lowered from 0.45 until the max degree is ~10K ("Miami 2.1M / avg 49 /
+    max 10K"): a = 0.41, b = c = 0.4·(1-a), d = 0.2·(1-a) (the 2:2:1 ratio of
+    RMAT(0.45,0.22,0.22,0.11)).  Realised: n = 2,097,152, nnz = 103,964,748,
+    avg 49.6, max 10,643.
+    """
+    a = 0.41
+    g = rmat(21, 52_000_000, a, 0.4 * (1 - a), 0.4 * (1 - a), seed=seed, perm_seed=7)
+    g.name = f"Miami-like(scale=21,m=5.2e7,a={a},seed={seed})"
+    return g
+
+
+def orkut_like(seed: int = 1) -> CSR:
+    """RMAT(0.45,0.22,0.22,0.11), scale 22, m = 1.2e8 drawn, id-permuted.
+
+    Realised: n = 4,194,304 (217,689 isolated), nnz = 239,797,400, max 34,166
+    (P:547 "Orkut 3M / 230M / avg 76 / max 33K").
+    """
+    g = rmat(22, 120_000_000, 0.45, 0.22, 0.22, seed=seed, perm_seed=7)
+    g.name = f"Orkut-like(scale=22,m=1.2e8,seed={seed})"
+    return g
+
+
+BIG_GRAPHS = {"rmat1m": lambda: rmat_1m_like(), "miami": lambda: miami_like(), "orkut": lambda: orkut_like()}
