@@ -1,0 +1,100 @@
+"""GPU parity at BASELINE.json's full sizes, in the launch configuration bench.py times.
+
+* Configs the CPU oracle can finish (u5-2, u7-2, u12-1 on RMAT-1M-like; u5-2, u7-2 on
+  Miami-like; u10-2 on Orkut-like): compared with oracle values written by
+  tools/make_golden_big.py (tests/golden/big_configs.json; calls only oracle/).
+  U64 bit-exact; F64 bit-exact below 2^53 else rel 1e-12; F32 rel 1e-4.
+* u15-1 (the bench workload) and u17 on RMAT-1M-like, where the oracle's dense
+  fp64 tables do not fit host RAM: properties that hold at any size (SURVEY §8(c)
+  pin 5): the exact U64 residue is the same for different roots / cut orders
+  (different kernels, index tables and schedules) and for the dense vs the
+  root-colour-anchored layout; F32 agrees with F64 to 1e-4.
+"""
+import json
+import math
+import os
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+import paper_2009_11665_b200 as sg  # noqa: E402
+from sg2v_inputs import BIG_GRAPHS, TEMPLATES  # noqa: E402
+
+GOLD = os.path.join(os.path.dirname(__file__), "golden", "big_configs.json")
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _dev():
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    torch.cuda.set_device(0)
+
+
+_graphs = {}
+
+
+def _graph(name):
+    if name not in _graphs:
+        _graphs.clear()
+        torch.cuda.empty_cache()
+        g = BIG_GRAPHS[name]()
+        _graphs[name] = (g, sg.graph_load_csr(g.n, g.row_offsets, g.col_indices))
+    return _graphs[name]
+
+
+def _k(e):
+    return 1 + max(max(x) for x in e)
+
+
+def _count(G, T, prec, layout="anchored", j=0):
+    ws = sg.Workspace(sg.workspace_bytes(G, T, prec, layout))
+    _, c = sg.count(G, T, n_iter=1, seed=1, iter_offset=j, precision=prec, workspace=ws,
+                    allow_overflow=True, layout=layout)
+    del ws
+    torch.cuda.empty_cache()
+    return c[0]
+
+
+CASES = json.load(open(GOLD))["cases"]
+
+
+@pytest.mark.parametrize("case", CASES, ids=[f"{c['graph']}-{c['template']}" for c in CASES])
+def test_big_config_vs_oracle(case):
+    g, G = _graph(case["graph"])
+    assert g.nnz == case["graph_stats"]["nnz"] and g.n == case["graph_stats"]["n"]
+    e = TEMPLATES[case["template"]]
+    T = sg.template_build(_k(e), e)
+    layouts = ("anchored", "dense") if case["k"] <= 7 else ("anchored",)
+    for layout in layouts:
+        assert int(_count(G, T, "u64", layout, case["j"])) == int(case["colorful_u64"]), layout
+        f64 = _count(G, T, "f64", layout, case["j"])
+        if case["max_intermediate"] < 2 ** 53:
+            assert f64 == case["colorful_f64"]
+        else:
+            assert math.isclose(f64, case["colorful_f64"], rel_tol=1e-12)
+        f32 = _count(G, T, "f32", layout, case["j"])
+        assert math.isfinite(f32) and math.isclose(f32, case["colorful_f64"], rel_tol=1e-4)
+
+
+def test_u15_bench_workload_invariants():
+    g, G = _graph("rmat1m")
+    e = TEMPLATES["u15-1"]
+    T = sg.template_build(15, e)                      # planner's root (bench plan)
+    ref = int(_count(G, T, "u64"))
+    assert int(_count(G, sg.template_build(15, e, root_hint=0), "u64")) == ref   # leaf-active chain
+    assert int(_count(G, T, "u64", "dense")) == ref                               # dense kernels
+    f64 = _count(G, T, "f64")
+    f32 = _count(G, T, "f32")                          # the bench's precision and layout
+    assert math.isfinite(f32) and math.isclose(f32, f64, rel_tol=1e-4)
+    assert f64 > 2 ** 53  # beyond fp64-exact territory: U64 is the exact check here
+
+
+def test_u17_invariants():
+    g, G = _graph("rmat1m")
+    e = TEMPLATES["u17"]
+    a = int(_count(G, sg.template_build(17, e), "u64"))
+    b = int(_count(G, sg.template_build(17, e, root_hint=5), "u64"))
+    assert a == b
