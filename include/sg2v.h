@@ -103,7 +103,11 @@ typedef struct {
     int32_t mode;             /* 0 = replicas (only mode implemented)                */
     void *nccl_comm;          /* reserved (vertex-partitioned mode), must be NULL    */
     int32_t device;           /* CUDA ordinal; -1 = current device                   */
-    uint64_t mem_budget_bytes;/* 0 = free device memory at call time                 */
+    uint64_t mem_budget_bytes;/* planning budget: the planner picks the fastest plan
+                                 whose workspace fits; 0 = device memory minus 6 GiB
+                                 (unlimited for host-only planning).  sg2v_count also
+                                 refuses (ENOMEM) a library-allocated workspace larger
+                                 than the free device memory                         */
     int32_t col_tile;         /* reserved, 0                                         */
     void *stream;             /* cudaStream_t (e.g. torch's current stream); NULL =
                                  legacy default stream                               */

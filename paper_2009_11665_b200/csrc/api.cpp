@@ -106,14 +106,34 @@ static Layout current_layout(int32_t lay) { return lay == 1 ? LAYOUT_DENSE : LAY
 
 static int32_t tls_layout() { return g_opts_init ? g_opts.layout : 0; }
 
+// Planning budget: the explicit mem_budget_bytes, else the device's total memory
+// minus a 6 GiB reserve (graph, context, allocator slack) — total, not free, so that
+// sg2v_workspace_bytes and sg2v_count agree on the plan — else unlimited (no device).
+static uint64_t plan_budget(uint64_t explicit_budget, int device) {
+    if (explicit_budget) return explicit_budget;
+    if (device < 0) return 0;
+    size_t fr = 0, tot = 0;
+    int cur = 0;
+    cudaGetDevice(&cur);
+    if (cur != device) cudaSetDevice(device);
+    cudaError_t e = cudaMemGetInfo(&fr, &tot);
+    if (cur != device) cudaSetDevice(cur);
+    if (e != cudaSuccess || tot == 0) return 0;
+    const uint64_t reserve = 6ull << 30;
+    return tot > reserve ? tot - reserve : tot;
+}
+
+static uint64_t tls_budget() { return g_opts_init ? g_opts.mem_budget_bytes : 0; }
+
 static sg2v_status get_plan(int64_t n, int64_t nnz, int device, const Template &t, sg2v_precision prec,
-                            int32_t layout, bool upload, Plan **out) {
+                            int32_t layout, bool upload, Plan **out, uint64_t explicit_budget = 0) {
     if (layout != 0 && layout != 1) { set_error("layout must be 0 (anchored) or 1 (dense)"); return SG2V_EINVAL; }
-    auto key = std::make_tuple((int)prec, n, nnz, device, (int)layout);
+    const uint64_t budget = plan_budget(explicit_budget, device);
+    auto key = std::make_tuple((int)prec, n, nnz, device, (int)layout, budget);
     auto &slot = const_cast<Template &>(t).plans[key];
     if (!slot) {
         std::unique_ptr<Plan> pl;
-        sg2v_status st = make_plan(t, n, nnz, prec, current_layout(layout), pl);
+        sg2v_status st = make_plan(t, n, nnz, prec, current_layout(layout), budget, pl);
         if (st != SG2V_OK) return st;
         slot = std::move(pl);
     }
@@ -258,7 +278,7 @@ sg2v_status sg2v_workspace_bytes(const sg2v_graph *g, const sg2v_template *t, sg
     if (prec < SG2V_F32 || prec > SG2V_U64) { set_error("bad precision"); return SG2V_EINVAL; }
     if (t->k == 1 || g->n == 0) { *bytes = 0; return SG2V_OK; }
     Plan *pl = nullptr;
-    sg2v_status st = get_plan(g->n, g->nnz, g->device, *t, prec, tls_layout(), false, &pl);
+    sg2v_status st = get_plan(g->n, g->nnz, g->device, *t, prec, tls_layout(), false, &pl, tls_budget());
     if (st != SG2V_OK) return st;
     *bytes = (uint64_t)pl->ws_bytes;
     return SG2V_OK;
@@ -279,7 +299,7 @@ sg2v_status sg2v_plan_describe_n(int64_t n, int64_t nnz, const sg2v_template *t,
         s = "{\"k\":" + std::to_string(t->k) + ",\"steps\":[],\"workspace_bytes\":0,\"alg_bytes\":0}";
     } else {
         Plan *pl = nullptr;
-        sg2v_status st = get_plan(n, nnz, -1, *t, prec, tls_layout(), false, &pl);
+        sg2v_status st = get_plan(n, nnz, -1, *t, prec, tls_layout(), false, &pl, tls_budget());
         if (st != SG2V_OK) return st;
         s = pl->describe();
     }
@@ -332,7 +352,7 @@ sg2v_status sg2v_count_ex(const sg2v_graph *g, const sg2v_template *t, int32_t k
         }
     } else {
         Plan *pl = nullptr;
-        st = get_plan(g->n, g->nnz, g->device, *t, o.precision, o.layout, true, &pl);
+        st = get_plan(g->n, g->nnz, g->device, *t, o.precision, o.layout, true, &pl, o.mem_budget_bytes);
         if (st != SG2V_OK) return st;
         char *ws = (char *)o.workspace;
         bool own = false;

@@ -489,9 +489,11 @@ static bool build_index(Plan &pl) {
     return true;
 }
 
+// Fastest modelled plan whose workspace fits `budget` (0 = unlimited); when no
+// plan fits, the smallest one (sg2v_count then reports ENOMEM with its size).
 sg2v_status make_plan(const Template &t, int64_t n, int64_t nnz, sg2v_precision prec, Layout layout,
-                      std::unique_ptr<Plan> &out) {
-    std::unique_ptr<Plan> best;
+                      uint64_t budget, std::unique_ptr<Plan> &out) {
+    std::unique_ptr<Plan> best, smallest;
     int r0 = 0, r1 = t.k - 1;
     if (t.root_hint >= 0) r0 = r1 = t.root_hint;
     for (int root = r0; root <= r1; ++root) {
@@ -499,11 +501,17 @@ sg2v_status make_plan(const Template &t, int64_t n, int64_t nnz, sg2v_precision 
             Chain c = build_chain(t, root, policy);
             auto pl = std::make_unique<Plan>();
             plan_chain(t, c, root, n, nnz, prec, layout, *pl);
+            const bool fits = budget == 0 || (uint64_t)pl->ws_bytes <= budget;
+            if (!smallest || pl->ws_bytes < smallest->ws_bytes) {
+                smallest = std::make_unique<Plan>(*pl);
+            }
+            if (!fits) continue;
             bool better = !best || pl->model_time < best->model_time * (1 - 1e-9) ||
                           (pl->model_time <= best->model_time * (1 + 1e-9) && pl->ws_bytes < best->ws_bytes);
             if (better) best = std::move(pl);
         }
     }
+    if (!best) best = std::move(smallest);
     if (!build_index(*best)) return SG2V_ENOMEM;
     out = std::move(best);
     return SG2V_OK;

@@ -104,7 +104,7 @@ struct Template {
     std::vector<std::vector<int>> adj;
     double alpha = 1.0;
     double P = 1.0;
-    std::map<std::tuple<int, int64_t, int64_t, int, int>, std::unique_ptr<Plan>> plans;
+    std::map<std::tuple<int, int64_t, int64_t, int, int, uint64_t>, std::unique_ptr<Plan>> plans;
     ~Template();
 };
 
@@ -112,7 +112,7 @@ struct Template {
 sg2v_status validate_template(int k, const int32_t *edges, Template &t);
 double automorphisms(const Template &t);
 sg2v_status make_plan(const Template &t, int64_t n, int64_t nnz, sg2v_precision prec, Layout layout,
-                      std::unique_ptr<Plan> &out);
+                      uint64_t budget, std::unique_ptr<Plan> &out);
 int64_t binom(int n, int r);
 
 // kernels.cu — launchers; all return cudaError_t as int (0 = success)

@@ -206,23 +206,24 @@ def template_build(k, edges, root_hint=-1) -> Template:
 LAYOUTS = {"anchored": 0, "dense": 1}
 
 
-def _set_layout(layout):
-    """Thread-local options carry the layout used by the planning queries."""
+def _set_layout(layout, mem_budget_bytes=0):
+    """Thread-local options carry the layout and budget used by the planning queries."""
     o = Options()
     lib().sg2v_options_default(ctypes.byref(o))
     o.layout = LAYOUTS[layout]
+    o.mem_budget_bytes = int(mem_budget_bytes)
     _check(lib().sg2v_set_options(ctypes.byref(o)))
 
 
-def workspace_bytes(graph: Graph, tmpl: Template, precision="f32", layout="anchored") -> int:
-    _set_layout(layout)
+def workspace_bytes(graph: Graph, tmpl: Template, precision="f32", layout="anchored", mem_budget_bytes=0) -> int:
+    _set_layout(layout, mem_budget_bytes)
     b = ctypes.c_uint64()
     _check(lib().sg2v_workspace_bytes(graph.handle, tmpl.handle, PRECISIONS[precision], ctypes.byref(b)))
     return int(b.value)
 
 
-def plan_describe(graph: Graph, tmpl: Template, precision="f32", layout="anchored") -> dict:
-    _set_layout(layout)
+def plan_describe(graph: Graph, tmpl: Template, precision="f32", layout="anchored", mem_budget_bytes=0) -> dict:
+    _set_layout(layout, mem_budget_bytes)
     need = ctypes.c_uint64()
     _check(lib().sg2v_plan_describe(graph.handle, tmpl.handle, PRECISIONS[precision], None, 0, ctypes.byref(need)))
     buf = ctypes.create_string_buffer(int(need.value))
@@ -231,9 +232,10 @@ def plan_describe(graph: Graph, tmpl: Template, precision="f32", layout="anchore
     return json.loads(buf.value.decode())
 
 
-def plan_describe_n(n: int, nnz: int, tmpl: Template, precision="f32", layout="anchored") -> dict:
+def plan_describe_n(n: int, nnz: int, tmpl: Template, precision="f32", layout="anchored",
+                    mem_budget_bytes=0) -> dict:
     """Host-only planning (no graph handle, no GPU)."""
-    _set_layout(layout)
+    _set_layout(layout, mem_budget_bytes)
     need = ctypes.c_uint64()
     _check(lib().sg2v_plan_describe_n(int(n), int(nnz), tmpl.handle, PRECISIONS[precision], None, 0,
                                       ctypes.byref(need)))
@@ -266,7 +268,7 @@ def count(graph: Graph, tmpl: Template, n_iter: int, seed: int, precision="f32",
     values of the last colouring.  layout: "anchored" (default) or "dense"."""
     prec = PRECISIONS[precision]
     if workspace is None and graph.n > 0 and tmpl.k > 1:
-        workspace = Workspace(workspace_bytes(graph, tmpl, precision, layout))
+        workspace = Workspace(workspace_bytes(graph, tmpl, precision, layout, mem_budget_bytes))
     o = Options()
     lib().sg2v_options_default(ctypes.byref(o))
     o.precision = prec

@@ -121,3 +121,16 @@ def test_no_cpu_fallback():
     with pytest.raises(sg.Sg2vError) as e:
         sg.graph_load_csr(3, np.array([0, 1, 2, 2]), np.array([1, 0], np.int32), stream=0)
     assert e.value.code == 4
+
+
+def test_planner_respects_memory_budget():
+    # u17 (random tree #1) on RMAT-1M-like in U64: the fastest plan needs ~169 GB;
+    # under a 150 GB budget the planner must pick a plan that fits
+    e = TEMPLATES["u17"]
+    T = sg.template_build(17, e)
+    free_plan = sg.plan_describe_n(1 << 20, 208_236_700, T, "u64")
+    capped = sg.plan_describe_n(1 << 20, 208_236_700, T, "u64", mem_budget_bytes=150 << 30)
+    assert capped["workspace_bytes"] <= 150 << 30 < free_plan["workspace_bytes"]
+    assert capped["model_seconds"] >= free_plan["model_seconds"]
+    tiny = sg.plan_describe_n(1 << 20, 208_236_700, T, "u64", mem_budget_bytes=1 << 30)
+    assert tiny["workspace_bytes"] > 1 << 30  # nothing fits: smallest plan (count -> ENOMEM)
