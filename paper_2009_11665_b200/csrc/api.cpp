@@ -123,6 +123,17 @@ static uint64_t plan_budget(uint64_t explicit_budget, int device) {
     return tot > reserve ? tot - reserve : tot;
 }
 
+static void keep_pool(int dev) {
+    static bool done[64] = {false};
+    if (dev < 0 || dev >= 64 || done[dev]) return;
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+        uint64_t thr = UINT64_MAX;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+    done[dev] = true;
+}
+
 static uint64_t tls_budget() { return g_opts_init ? g_opts.mem_budget_bytes : 0; }
 
 static sg2v_status get_plan(int64_t n, int64_t nnz, int device, const Template &t, sg2v_precision prec,
@@ -198,10 +209,14 @@ sg2v_status sg2v_graph_load_csr(int64_t n, const int64_t *row_offsets, const int
     cudaStream_t s = (cudaStream_t)o.stream;
     auto fail = [&](sg2v_status code) { sg2v_graph_free(g); return code; };
     cudaError_t e;
-    if ((e = cudaMalloc(&g->d_rowptr, (n + 1) * sizeof(int64_t))) != cudaSuccess) return fail(cuda_fail("cudaMalloc rowptr", e));
-    if ((e = cudaMalloc(&g->d_col, std::max<int64_t>(nnz, 1) * sizeof(int32_t))) != cudaSuccess) return fail(cuda_fail("cudaMalloc col", e));
-    if ((e = cudaMalloc(&g->d_order, std::max<int64_t>(n, 1) * sizeof(int32_t))) != cudaSuccess) return fail(cuda_fail("cudaMalloc order", e));
-    if ((e = cudaMalloc(&g->d_vclass, std::max<int64_t>(n, 1))) != cudaSuccess) return fail(cuda_fail("cudaMalloc vclass", e));
+    // stream-ordered allocations from the device's default pool, which keeps freed
+    // memory mapped (release threshold = max): repeated load/free cycles cost no
+    // page-table work (the e2e path of bench.py)
+    keep_pool(dev);
+    if ((e = cudaMallocAsync((void **)&g->d_rowptr, (n + 1) * sizeof(int64_t), s)) != cudaSuccess) return fail(cuda_fail("cudaMallocAsync rowptr", e));
+    if ((e = cudaMallocAsync((void **)&g->d_col, std::max<int64_t>(nnz, 1) * sizeof(int32_t), s)) != cudaSuccess) return fail(cuda_fail("cudaMallocAsync col", e));
+    if ((e = cudaMallocAsync((void **)&g->d_order, std::max<int64_t>(n, 1) * sizeof(int32_t), s)) != cudaSuccess) return fail(cuda_fail("cudaMallocAsync order", e));
+    if ((e = cudaMallocAsync((void **)&g->d_vclass, std::max<int64_t>(n, 1), s)) != cudaSuccess) return fail(cuda_fail("cudaMallocAsync vclass", e));
     cudaMemcpyKind kind = dev_ptrs ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
     if ((e = cudaMemcpyAsync(g->d_rowptr, row_offsets, (n + 1) * sizeof(int64_t), kind, s)) != cudaSuccess) return fail(cuda_fail("copy rowptr", e));
     if (nnz > 0 && (e = cudaMemcpyAsync(g->d_col, col_indices, nnz * sizeof(int32_t), kind, s)) != cudaSuccess) return fail(cuda_fail("copy col", e));
@@ -238,10 +253,11 @@ void sg2v_graph_free(sg2v_graph *g) {
     int cur = 0;
     cudaGetDevice(&cur);
     cudaSetDevice(g->device);
-    cudaFree(g->d_rowptr);
-    cudaFree(g->d_col);
-    cudaFree(g->d_order);
-    cudaFree(g->d_vclass);
+    // stream-ordered on the legacy default stream (ordered after work on blocking streams)
+    if (g->d_rowptr) cudaFreeAsync(g->d_rowptr, 0);
+    if (g->d_col) cudaFreeAsync(g->d_col, 0);
+    if (g->d_order) cudaFreeAsync(g->d_order, 0);
+    if (g->d_vclass) cudaFreeAsync(g->d_vclass, 0);
     cudaSetDevice(cur);
     delete g;
 }
@@ -370,10 +386,11 @@ sg2v_status sg2v_count_ex(const sg2v_graph *g, const sg2v_template *t, int32_t k
                           std::to_string(budget));
                 return SG2V_ENOMEM;
             }
-            SG2V_CK(cudaMalloc(&ws, pl->ws_bytes));
+            keep_pool(dev);
+            SG2V_CK(cudaMallocAsync((void **)&ws, pl->ws_bytes, s));
             own = true;
         }
-        struct Free { char *p; bool own; ~Free() { if (own) cudaFree(p); } } freer{ws, own};
+        struct Free { char *p; bool own; cudaStream_t s; ~Free() { if (own) cudaFreeAsync(p, s); } } freer{ws, own, s};
         if (o.mem_budget_bytes && (uint64_t)pl->ws_bytes > o.mem_budget_bytes) {
             set_error("ENOMEM: plan needs " + std::to_string(pl->ws_bytes) + " bytes, budget " +
                       std::to_string(o.mem_budget_bytes));

@@ -453,23 +453,23 @@ int graph_build_order(Graph &g, void *stream) {
     int32_t *deg = nullptr, *deg_sorted = nullptr, *ids = nullptr;
     void *tmp = nullptr;
     size_t tmp_bytes = 0;
-    cudaError_t e = cudaMalloc(&deg, n * sizeof(int32_t) * 3);
+    cudaError_t e = cudaMallocAsync((void **)&deg, n * sizeof(int32_t) * 3, s);
     if (e != cudaSuccess) return (int)e;
     deg_sorted = deg + n;
     ids = deg + 2 * n;
     degree_kernel<<<(unsigned)std::min<int64_t>((n + 255) / 256, 4096), 256, 0, s>>>(n, g.d_rowptr, deg, ids);
     cub::DeviceRadixSort::SortPairsDescending(nullptr, tmp_bytes, deg, deg_sorted, ids, g.d_order, (int)n, 0, 32, s);
-    e = cudaMalloc(&tmp, tmp_bytes);
+    e = cudaMallocAsync(&tmp, tmp_bytes, s);
     if (e == cudaSuccess) {
         cub::DeviceRadixSort::SortPairsDescending(tmp, tmp_bytes, deg, deg_sorted, ids, g.d_order, (int)n, 0, 32, s);
         vclass_kernel<<<(unsigned)std::min<int64_t>((n + 255) / 256, 4096), 256, 0, s>>>(n, g.d_order, g.d_vclass);
         int32_t mx = 0;
         cudaMemcpyAsync(&mx, deg_sorted, sizeof(int32_t), cudaMemcpyDeviceToHost, s);
+        cudaFreeAsync(tmp, s);
         e = cudaStreamSynchronize(s);
         g.max_deg = mx;
-        cudaFree(tmp);
     }
-    cudaFree(deg);
+    cudaFreeAsync(deg, s);
     if (e != cudaSuccess) return (int)e;
     return (int)cudaGetLastError();
 }
