@@ -159,6 +159,25 @@ sg2v_status sg2v_count_ex(const sg2v_graph *g, const sg2v_template *t, int32_t k
                           uint64_t *colorful_u64_out);
 
 /*
+ * sg2v_count_batch — m templates of the same size k on the SAME colourings
+ * (treelet distributions, Fig. 1): the colouring and the
+ * colour buckets / histogram are computed once per colouring and shared, then
+ * each template's DP runs in turn in one workspace (tables of consecutive
+ * templates reuse the same arena).
+ *   templates      array of m template handles, all with k vertices (EINVAL otherwise)
+ *   estimates_out  double[m] or NULL;  colorful_out / colorful_u64_out:
+ *                  [m * n_iter], template-major (entry t*n_iter + q), or NULL.
+ * Values are identical to m separate sg2v_count calls with the same options.
+ */
+sg2v_status sg2v_count_batch(const sg2v_graph *g, const sg2v_template *const *templates, int32_t m,
+                             int32_t k, int64_t n_iter, uint64_t seed, const sg2v_options *o,
+                             double *estimates_out, double *colorful_out,
+                             uint64_t *colorful_u64_out);
+/* Workspace bytes of sg2v_count_batch (thread-local layout / budget options). */
+sg2v_status sg2v_workspace_bytes_batch(const sg2v_graph *g, const sg2v_template *const *templates,
+                                       int32_t m, sg2v_precision precision, uint64_t *bytes);
+
+/*
  * sg2v_colorize — kernel a1 alone: writes
  * COLOR(seed, j, v, k) for v in [0,n) to the DEVICE array colors_out (uint8[n])
  * on `stream` (cudaStream_t or NULL).  For parity tests of the colouring.

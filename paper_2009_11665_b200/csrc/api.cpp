@@ -335,11 +335,67 @@ sg2v_status sg2v_colorize(uint64_t seed, int64_t j, int64_t n, int32_t k, uint8_
     return SG2V_OK;
 }
 
-sg2v_status sg2v_count_ex(const sg2v_graph *g, const sg2v_template *t, int32_t k, int64_t n_iter, uint64_t seed,
-                          const sg2v_options *op, double *estimate_out, double *colorful_out,
-                          uint64_t *colorful_u64_out) {
-    if (!g || !t) { set_error("graph or template is NULL"); return SG2V_EINVAL; }
-    if (k != t->k) { set_error("k must equal the number of template vertices (P:161)"); return SG2V_EINVAL; }
+}  // extern "C"
+
+namespace sg2v {
+
+// Workspace of a batch of m same-k templates run on every colouring: the table
+// arenas overlap (templates run one after another), the per-colouring buffers
+// (colours, histogram / colour buckets, row values) are shared.  For m = 1 this
+// is exactly the plan's own layout (Plan::ws_bytes).
+struct BatchLayout {
+    int64_t off_colors = 0, off_hist = 0, off_hcnt = 0, off_bcol = 0, off_rowval = 0, off_partial = 0,
+            off_results = 0, bytes = 0;
+};
+
+static int64_t rup(int64_t x, int64_t m) { return (x + m - 1) / m * m; }
+
+static BatchLayout batch_layout(const std::vector<Plan *> &pls, int64_t n, int64_t nnz) {
+    BatchLayout L;
+    int64_t tables = 0, hist = 0;
+    bool anch = false;
+    for (Plan *p : pls) {
+        tables = std::max(tables, p->tables_bytes);
+        hist = std::max(hist, p->hist_bytes);
+        anch = anch || p->layout == LAYOUT_ANCHORED;
+    }
+    const int64_t kp = pls.empty() ? 0 : pls[0]->kp;
+    int64_t off = rup(tables, 256);
+    L.off_colors = off;  off = rup(off + std::max<int64_t>(n, 1) + 16, 256);
+    L.off_hist = off;    off = rup(off + hist, 256);
+    L.off_hcnt = off;    off = rup(off + (anch ? n * kp * 4 : 0), 256);
+    L.off_bcol = off;    off = rup(off + (anch ? nnz * 4 : 0), 256);
+    L.off_rowval = off;  off = rup(off + std::max<int64_t>(n, 1) * 8, 256);
+    L.off_partial = off; off = rup(off + kReduceBlocks * 8, 256);
+    L.off_results = off; off = rup(off + (int64_t)kResultsRing * 8 * (int64_t)std::max<size_t>(pls.size(), 1), 256);
+    L.bytes = off;
+    return L;
+}
+
+static sg2v_status batch_plans(const sg2v_graph *g, const sg2v_template *const *ts, int32_t m, sg2v_precision prec,
+                               int32_t layout, bool upload, uint64_t budget, std::vector<Plan *> &pls) {
+    pls.clear();
+    for (int32_t q = 0; q < m; ++q) {
+        if (ts[q]->k == 1 || g->n == 0) continue;
+        Plan *pl = nullptr;
+        sg2v_status st = get_plan(g->n, g->nnz, g->device, *ts[q], prec, layout, upload, &pl, budget);
+        if (st != SG2V_OK) return st;
+        pls.push_back(pl);
+    }
+    return SG2V_OK;
+}
+
+// Alg. 1 / Alg. 5 outer loop for m templates sharing every colouring (a1 and the
+// colour buckets / histogram once per colouring).
+// colorful[m * n_iter] / colorful_u64[m * n_iter] template-major.
+static sg2v_status count_core(const sg2v_graph *g, const sg2v_template *const *ts, int32_t m, int32_t k,
+                              int64_t n_iter, uint64_t seed, const sg2v_options *op, double *estimates,
+                              double *colorful_out, uint64_t *colorful_u64_out) {
+    if (!g || !ts || m < 1) { set_error("graph or templates NULL / m < 1"); return SG2V_EINVAL; }
+    for (int32_t q = 0; q < m; ++q) {
+        if (!ts[q]) { set_error("template is NULL"); return SG2V_EINVAL; }
+        if (ts[q]->k != k) { set_error("k must equal the number of template vertices of every template (P:161)"); return SG2V_EINVAL; }
+    }
     if (n_iter <= 0) { set_error("n_iter must be >= 1"); return SG2V_EINVAL; }
     sg2v_options o;
     if (op) o = *op; else if (g_opts_init) o = g_opts; else sg2v_options_default(&o);
@@ -353,13 +409,14 @@ sg2v_status sg2v_count_ex(const sg2v_graph *g, const sg2v_template *t, int32_t k
     if (st != SG2V_OK) return st;
     struct Restore { int d; ~Restore() { cudaSetDevice(d); } } restore{prev_dev};
     const bool u64mode = o.precision == SG2V_U64;
-    std::vector<double> resf(n_iter, 0.0);
-    std::vector<uint64_t> resu(n_iter, 0);
+    std::vector<double> resf((size_t)m * n_iter, 0.0);
+    std::vector<uint64_t> resu((size_t)m * n_iter, 0);
     cudaStream_t s = (cudaStream_t)o.stream;
 
     if (k == 1 || g->n == 0) {
         // single-vertex template: every vertex is a colourful embedding; empty graph: 0
-        for (int64_t q = 0; q < n_iter; ++q) { resf[q] = (double)g->n; resu[q] = (uint64_t)g->n; }
+        for (auto &x : resf) x = (double)g->n;
+        for (auto &x : resu) x = (uint64_t)g->n;
         if (o.row_values && g->n > 0) {
             std::vector<uint64_t> ones_u(g->n, 1);
             std::vector<double> ones_f(g->n, 1.0);
@@ -367,70 +424,79 @@ sg2v_status sg2v_count_ex(const sg2v_graph *g, const sg2v_template *t, int32_t k
             SG2V_CK(cudaMemcpy(o.row_values, srcp, g->n * 8, cudaMemcpyHostToDevice));
         }
     } else {
-        Plan *pl = nullptr;
-        st = get_plan(g->n, g->nnz, g->device, *t, o.precision, o.layout, true, &pl, o.mem_budget_bytes);
+        std::vector<Plan *> pls;
+        st = batch_plans(g, ts, m, o.precision, o.layout, true, o.mem_budget_bytes, pls);
         if (st != SG2V_OK) return st;
+        const BatchLayout L = batch_layout(pls, g->n, g->nnz);
         char *ws = (char *)o.workspace;
         bool own = false;
         if (ws) {
-            if (o.workspace_bytes < (uint64_t)pl->ws_bytes) {
-                set_error("workspace too small: need " + std::to_string(pl->ws_bytes) + " bytes");
+            if (o.workspace_bytes < (uint64_t)L.bytes) {
+                set_error("workspace too small: need " + std::to_string(L.bytes) + " bytes");
                 return SG2V_ENOMEM;
             }
         } else {
             size_t fr = 0, tot = 0;
             cudaMemGetInfo(&fr, &tot);
             uint64_t budget = o.mem_budget_bytes ? o.mem_budget_bytes : (uint64_t)fr;
-            if ((uint64_t)pl->ws_bytes > budget) {
-                set_error("ENOMEM: plan needs " + std::to_string(pl->ws_bytes) + " bytes of device memory, budget " +
+            if ((uint64_t)L.bytes > budget) {
+                set_error("ENOMEM: plan needs " + std::to_string(L.bytes) + " bytes of device memory, budget " +
                           std::to_string(budget));
                 return SG2V_ENOMEM;
             }
             keep_pool(dev);
-            SG2V_CK(cudaMallocAsync((void **)&ws, pl->ws_bytes, s));
+            SG2V_CK(cudaMallocAsync((void **)&ws, L.bytes, s));
             own = true;
         }
         struct Free { char *p; bool own; cudaStream_t s; ~Free() { if (own) cudaFreeAsync(p, s); } } freer{ws, own, s};
-        if (o.mem_budget_bytes && (uint64_t)pl->ws_bytes > o.mem_budget_bytes) {
-            set_error("ENOMEM: plan needs " + std::to_string(pl->ws_bytes) + " bytes, budget " +
+        if (o.mem_budget_bytes && (uint64_t)L.bytes > o.mem_budget_bytes) {
+            set_error("ENOMEM: plan needs " + std::to_string(L.bytes) + " bytes, budget " +
                       std::to_string(o.mem_budget_bytes));
             return SG2V_ENOMEM;
         }
-        uint8_t *colors = (uint8_t *)(ws + pl->off_colors);
-        void *H = ws + pl->off_hist;
-        void *rowval = ws + pl->off_rowval;
-        void *partial = ws + pl->off_partial;
-        char *results = ws + pl->off_results;
-        int32_t *hcnt = (int32_t *)(ws + pl->off_hcnt);
-        int32_t *bcol = (int32_t *)(ws + pl->off_bcol);
-        const bool anch = pl->layout == LAYOUT_ANCHORED;
-        std::vector<uint64_t> host_ring(kResultsRing);
+        uint8_t *colors = (uint8_t *)(ws + L.off_colors);
+        void *H = ws + L.off_hist;
+        void *rowval = ws + L.off_rowval;
+        void *partial = ws + L.off_partial;
+        char *results = ws + L.off_results;
+        int32_t *hcnt = (int32_t *)(ws + L.off_hcnt);
+        int32_t *bcol = (int32_t *)(ws + L.off_bcol);
+        const bool anch = pls[0]->layout == LAYOUT_ANCHORED;
+        bool need_hist = false;
+        for (Plan *p : pls) need_hist = need_hist || p->need_hist;
+        std::vector<uint64_t> host_ring((size_t)kResultsRing * m);
         int64_t base = 0;
         for (int64_t q = 0; q < n_iter; ++q) {
             const int64_t j = o.iter_offset + q * o.iter_stride;
             int rc = launch_colorize(seed, j, g->n, k, colors, s);
             if (rc) return cuda_fail("colorize", rc);
-            if (pl->need_hist && (rc = launch_hist(*g, *pl, colors, H, s))) return cuda_fail("hist", rc);
-            if (anch && (rc = launch_bucket(*g, *pl, colors, hcnt, bcol, s))) return cuda_fail("bucket", rc);
-            for (const Step &stp : pl->steps) {
-                rc = anch ? launch_astep(*g, *pl, stp, colors, hcnt, bcol, ws, rowval, s)
-                          : launch_step(*g, *pl, stp, colors, H, ws, rowval, s);
-                if (rc == -1) {
-                    set_error("row too wide for on-chip B (shared memory > 227 KB)");
-                    return SG2V_ENOMEM;
+            if (need_hist && (rc = launch_hist(*g, *pls[0], colors, H, s))) return cuda_fail("hist", rc);
+            if (anch && (rc = launch_bucket(*g, *pls[0], colors, hcnt, bcol, s))) return cuda_fail("bucket", rc);
+            for (int32_t tq = 0; tq < m; ++tq) {
+                const Plan *pl = pls[tq];
+                for (const Step &stp : pl->steps) {
+                    rc = anch ? launch_astep(*g, *pl, stp, colors, hcnt, bcol, ws, rowval, s)
+                              : launch_step(*g, *pl, stp, colors, H, ws, rowval, s);
+                    if (rc == -1) {
+                        set_error("row too wide for on-chip B (shared memory > 227 KB)");
+                        return SG2V_ENOMEM;
+                    }
+                    if (rc) return cuda_fail("step", rc);
                 }
-                if (rc) return cuda_fail("step", rc);
+                rc = launch_reduce(*pl, g->n, rowval, partial, results + ((q - base) * m + tq) * 8, s);
+                if (rc) return cuda_fail("reduce", rc);
             }
-            rc = launch_reduce(*pl, g->n, rowval, partial, results + (q - base) * 8, s);
-            if (rc) return cuda_fail("reduce", rc);
             if (q - base + 1 == kResultsRing || q == n_iter - 1) {
                 int64_t cnt = q - base + 1;
-                SG2V_CK(cudaMemcpyAsync(host_ring.data(), results, cnt * 8, cudaMemcpyDeviceToHost, s));
+                SG2V_CK(cudaMemcpyAsync(host_ring.data(), results, cnt * m * 8, cudaMemcpyDeviceToHost, s));
                 SG2V_CK(cudaStreamSynchronize(s));
-                for (int64_t r = 0; r < cnt; ++r) {
-                    if (u64mode) resu[base + r] = host_ring[r];
-                    else std::memcpy(&resf[base + r], &host_ring[r], 8);
-                }
+                for (int64_t r = 0; r < cnt; ++r)
+                    for (int32_t tq = 0; tq < m; ++tq) {
+                        const uint64_t bits = host_ring[(size_t)(r * m + tq)];
+                        const size_t dst = (size_t)tq * n_iter + (size_t)(base + r);
+                        if (u64mode) resu[dst] = bits;
+                        else std::memcpy(&resf[dst], &bits, 8);
+                    }
                 base = q + 1;
             }
         }
@@ -440,21 +506,55 @@ sg2v_status sg2v_count_ex(const sg2v_graph *g, const sg2v_template *t, int32_t k
         }
     }
     bool finite = true;
-    double sum = 0.0;
-    for (int64_t q = 0; q < n_iter; ++q) {
-        if (colorful_out) colorful_out[q] = u64mode ? (double)resu[q] : resf[q];
-        if (colorful_u64_out) colorful_u64_out[q] = u64mode ? resu[q] : (uint64_t)resf[q];
-        if (!u64mode) {
-            if (!std::isfinite(resf[q])) finite = false;
-            sum += resf[q];
+    for (int32_t tq = 0; tq < m; ++tq) {
+        double sum = 0.0;
+        for (int64_t q = 0; q < n_iter; ++q) {
+            const size_t at = (size_t)tq * n_iter + (size_t)q;
+            if (colorful_out) colorful_out[at] = u64mode ? (double)resu[at] : resf[at];
+            if (colorful_u64_out) colorful_u64_out[at] = u64mode ? resu[at] : (uint64_t)resf[at];
+            if (!u64mode) {
+                if (!std::isfinite(resf[at])) finite = false;
+                sum += resf[at];
+            }
         }
+        if (estimates)
+            estimates[tq] = u64mode ? std::nan("") : sum / (double)n_iter / (ts[tq]->P * ts[tq]->alpha);
     }
-    if (estimate_out)
-        *estimate_out = u64mode ? std::nan("") : sum / (double)n_iter / (t->P * t->alpha);
     if (!finite) {
         set_error("EOVERFLOW: a colourful count is not finite in F32 (use F64 or U64)");
         return SG2V_EOVERFLOW;
     }
+    return SG2V_OK;
+}
+
+}  // namespace sg2v
+
+extern "C" {
+
+sg2v_status sg2v_count_ex(const sg2v_graph *g, const sg2v_template *t, int32_t k, int64_t n_iter, uint64_t seed,
+                          const sg2v_options *op, double *estimate_out, double *colorful_out,
+                          uint64_t *colorful_u64_out) {
+    if (!t) { set_error("graph or template is NULL"); return SG2V_EINVAL; }
+    const sg2v_template *ts[1] = {t};
+    return count_core(g, ts, 1, k, n_iter, seed, op, estimate_out, colorful_out, colorful_u64_out);
+}
+
+sg2v_status sg2v_count_batch(const sg2v_graph *g, const sg2v_template *const *templates, int32_t m, int32_t k,
+                             int64_t n_iter, uint64_t seed, const sg2v_options *o, double *estimates_out,
+                             double *colorful_out, uint64_t *colorful_u64_out) {
+    return count_core(g, templates, m, k, n_iter, seed, o, estimates_out, colorful_out, colorful_u64_out);
+}
+
+sg2v_status sg2v_workspace_bytes_batch(const sg2v_graph *g, const sg2v_template *const *templates, int32_t m,
+                                       sg2v_precision prec, uint64_t *bytes) {
+    if (!g || !templates || m < 1 || !bytes) { set_error("NULL argument"); return SG2V_EINVAL; }
+    if (prec < SG2V_F32 || prec > SG2V_U64) { set_error("bad precision"); return SG2V_EINVAL; }
+    for (int32_t q = 0; q < m; ++q)
+        if (!templates[q]) { set_error("template is NULL"); return SG2V_EINVAL; }
+    std::vector<Plan *> pls;
+    sg2v_status st = batch_plans(g, templates, m, prec, tls_layout(), false, tls_budget(), pls);
+    if (st != SG2V_OK) return st;
+    *bytes = pls.empty() ? 0 : (uint64_t)batch_layout(pls, g->n, g->nnz).bytes;
     return SG2V_OK;
 }
 

@@ -53,7 +53,8 @@ _lib = None
 SYMBOLS = ["sg2v_graph_load_csr", "sg2v_graph_free", "sg2v_template_build", "sg2v_template_free",
            "sg2v_template_info", "sg2v_options_default", "sg2v_set_options", "sg2v_workspace_bytes",
            "sg2v_count", "sg2v_count_ex", "sg2v_colorize", "sg2v_plan_describe", "sg2v_plan_describe_n", "sg2v_profile_enable",
-           "sg2v_profile_read", "sg2v_last_error", "sg2v_version"]
+           "sg2v_profile_read", "sg2v_last_error", "sg2v_version", "sg2v_count_batch",
+           "sg2v_workspace_bytes_batch"]
 
 
 def lib():
@@ -79,6 +80,8 @@ def lib():
         L.sg2v_count.argtypes = [vp, vp, i32, i64, u64, vp, vp, vp]
         L.sg2v_count_ex.argtypes = [vp, vp, i32, i64, u64, P(Options), vp, vp, vp]
         L.sg2v_colorize.argtypes = [u64, i64, i64, i32, vp, vp]
+        L.sg2v_count_batch.argtypes = [vp, vp, i32, i32, i64, u64, P(Options), vp, vp, vp]
+        L.sg2v_workspace_bytes_batch.argtypes = [vp, vp, i32, ctypes.c_int, P(u64)]
         L.sg2v_plan_describe.argtypes = [vp, vp, ctypes.c_int, vp, u64, P(u64)]
         L.sg2v_plan_describe_n.argtypes = [i64, i64, vp, ctypes.c_int, vp, u64, P(u64)]
         L.sg2v_profile_enable.argtypes = [i32]
@@ -87,7 +90,8 @@ def lib():
         L.sg2v_version.restype = ctypes.c_char_p
         for name in ("sg2v_graph_load_csr", "sg2v_template_build", "sg2v_template_info", "sg2v_set_options",
                      "sg2v_workspace_bytes", "sg2v_count", "sg2v_count_ex", "sg2v_colorize",
-                     "sg2v_plan_describe", "sg2v_plan_describe_n", "sg2v_profile_enable", "sg2v_profile_read"):
+                     "sg2v_plan_describe", "sg2v_plan_describe_n", "sg2v_profile_enable", "sg2v_profile_read",
+                     "sg2v_count_batch", "sg2v_workspace_bytes_batch"):
             getattr(L, name).restype = ctypes.c_int
         _lib = L
     return _lib
@@ -295,6 +299,56 @@ def count(graph: Graph, tmpl: Template, n_iter: int, seed: int, precision="f32",
         return est.value, out
     _check(rc)
     return est.value, out
+
+
+def _handles(tmpls):
+    arr = (ctypes.c_void_p * len(tmpls))(*[t.handle for t in tmpls])
+    return arr
+
+
+def workspace_bytes_batch(graph: Graph, tmpls, precision="f32", layout="anchored", mem_budget_bytes=0) -> int:
+    _set_layout(layout, mem_budget_bytes)
+    b = ctypes.c_uint64()
+    _check(lib().sg2v_workspace_bytes_batch(graph.handle, _handles(tmpls), len(tmpls), PRECISIONS[precision],
+                                            ctypes.byref(b)))
+    return int(b.value)
+
+
+def count_batch(graph: Graph, tmpls, n_iter: int, seed: int, precision="f32", iter_offset=0, iter_stride=1,
+                workspace: Workspace | None = None, stream=None, allow_overflow=False, mem_budget_bytes=0,
+                layout="anchored"):
+    """sg2v_count_batch: m same-size templates on the same colourings.
+    Returns (estimates[m], colorful[m, n_iter])."""
+    m = len(tmpls)
+    k = tmpls[0].k
+    prec = PRECISIONS[precision]
+    if workspace is None and graph.n > 0 and k > 1:
+        workspace = Workspace(workspace_bytes_batch(graph, tmpls, precision, layout, mem_budget_bytes))
+    o = Options()
+    lib().sg2v_options_default(ctypes.byref(o))
+    o.precision = prec
+    o.iter_offset = int(iter_offset)
+    o.iter_stride = int(iter_stride)
+    o.stream = stream if stream is not None else _cur_stream()
+    o.mem_budget_bytes = int(mem_budget_bytes)
+    o.layout = LAYOUTS[layout]
+    if workspace is not None:
+        o.workspace = workspace.ptr
+        o.workspace_bytes = workspace.nbytes
+    est = np.zeros(m, dtype=np.float64)
+    hs = _handles(tmpls)
+    if prec == U64:
+        out = np.zeros((m, n_iter), dtype=np.uint64)
+        rc = lib().sg2v_count_batch(graph.handle, hs, m, k, int(n_iter), int(seed) & (2**64 - 1), ctypes.byref(o),
+                                    est.ctypes.data, None, out.ctypes.data)
+    else:
+        out = np.zeros((m, n_iter), dtype=np.float64)
+        rc = lib().sg2v_count_batch(graph.handle, hs, m, k, int(n_iter), int(seed) & (2**64 - 1), ctypes.byref(o),
+                                    est.ctypes.data, out.ctypes.data, None)
+    if rc == EOVERFLOW and allow_overflow:
+        return est, out
+    _check(rc)
+    return est, out
 
 
 def colorize(seed, j, n, k, out, stream=None):

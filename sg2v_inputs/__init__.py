@@ -28,4 +28,5 @@ from .templates import (  # noqa: F401
     path_template,
     star_template,
     random_tree,
+    all_trees,
 )

@@ -84,3 +84,63 @@ def template_edges(name: str):
     e = TEMPLATES[name]
     k = 1 + max((max(a, b) for a, b in e), default=0)
     return k, list(e)
+
+
+def _canon_free(k, edges):
+    """Canonical string of an unrooted tree (centre + AHU nesting) for dedupe."""
+    adj = [[] for _ in range(k)]
+    for a, b in edges:
+        adj[a].append(b)
+        adj[b].append(a)
+
+    def enc(v, p):
+        return "(" + "".join(sorted(enc(c, v) for c in adj[v] if c != p)) + ")"
+    if k <= 2:
+        return str(k)
+    deg = [len(x) for x in adj]
+    layer = [v for v in range(k) if deg[v] == 1]
+    left = k
+    while left > 2:
+        left -= len(layer)
+        nxt = []
+        for v in layer:
+            for u in adj[v]:
+                deg[u] -= 1
+                if deg[u] == 1:
+                    nxt.append(u)
+        layer = nxt
+    if len(layer) == 1:
+        return enc(layer[0], -1)
+    a, b = layer
+    return "".join(sorted([enc(a, b), enc(b, a)]))
+
+
+def all_trees(k: int):
+    """Every non-isomorphic tree on k vertices (k <= 9), as edge lists, in a fixed
+    order (Prüfer enumeration, first representative of each isomorphism class).
+    Counts: 1, 1, 1, 2, 3, 6, 11, 23, 47 (the paper's 47 size-9 treelets)."""
+    import itertools
+    if k == 1:
+        return [[]]
+    if k == 2:
+        return [[(0, 1)]]
+    seen, out = set(), []
+    for seq in itertools.product(range(k), repeat=k - 2):
+        degree = [1] * k
+        for x in seq:
+            degree[x] += 1
+        edges = []
+        for x in seq:
+            for leaf in range(k):
+                if degree[leaf] == 1:
+                    edges.append((min(leaf, x), max(leaf, x)))
+                    degree[leaf] -= 1
+                    degree[x] -= 1
+                    break
+        u, v = [i for i in range(k) if degree[i] == 1]
+        edges.append((u, v))
+        c = _canon_free(k, edges)
+        if c not in seen:
+            seen.add(c)
+            out.append(sorted(edges))
+    return out

@@ -251,3 +251,59 @@ def test_f32_close_to_f64_on_dense_graph():
     _, f = sg.count(G, T, n_iter=1, seed=1, precision="f32")
     _, d = sg.count(G, T, n_iter=1, seed=1, precision="f64")
     assert math.isclose(f[0], d[0], rel_tol=1e-4)
+
+
+# --------------------------------------------------------------------------- multi-template batch
+def test_count_batch_equals_single_counts(oracle):
+    from sg2v_inputs import all_trees
+    g = rmat(11, 30_000, 0.45, 0.22, 0.22, seed=8)
+    G = _load(g)
+    trees = all_trees(6)
+    Ts = [sg.template_build(6, e) for e in trees]
+    for layout in LAYOUTS:
+        est, col = sg.count_batch(G, Ts, n_iter=3, seed=4, precision="u64", layout=layout)
+        for t, e in enumerate(trees):
+            _, one = sg.count(G, Ts[t], n_iter=3, seed=4, precision="u64", layout=layout)
+            assert np.array_equal(col[t], one)
+            assert int(col[t][1]) == oracle.count(g, 6, e, oracle.colors(4, 1, g.n, 6))
+        estf, colf = sg.count_batch(G, Ts, n_iter=3, seed=4, precision="f64", layout=layout)
+        for t in range(len(trees)):
+            _, onef = sg.count(G, Ts[t], n_iter=3, seed=4, precision="f64", layout=layout)
+            assert np.array_equal(colf[t], onef)
+    with pytest.raises(sg.Sg2vError):
+        sg.count_batch(G, [Ts[0], sg.template_build(5, TEMPLATES["u5-2"])], n_iter=1, seed=1)
+
+
+def test_fig1_analogue_treelet_distributions():
+    # SPEC S:540 / P:107-117: distributions over the 11 size-7 trees separate two
+    # structurally different random-graph models more than two samples of one model
+    from paper_2009_11665_b200.estimator import compare_distributions, estimate_distribution
+    from sg2v_inputs import all_trees, csr_from_edges
+    trees = all_trees(7)
+    Ts = [sg.template_build(7, e) for e in trees]
+
+    def regular(seed, n=500, d=6):
+        rng = np.random.default_rng(seed)
+        stubs = np.repeat(np.arange(n), d)
+        rng.shuffle(stubs)
+        return csr_from_edges(n, stubs[0::2], stubs[1::2])
+
+    def pref_attach(seed, n=500, m=3):
+        rng = np.random.default_rng(seed)
+        us, vs, targets = [], [], list(range(m))
+        for v in range(m, n):
+            pick = rng.choice(targets, size=m, replace=True)
+            for u in pick:
+                us.append(v)
+                vs.append(int(u))
+            targets += list(pick) + [v] * m
+        return csr_from_edges(n, us, vs)
+
+    dists = []
+    for g in (regular(1), regular(2), pref_attach(1), pref_attach(2)):
+        d, _, _ = estimate_distribution(_load(g), Ts, n_iter=200, seed=3, precision="f64")
+        dists.append(d)
+    D = compare_distributions(dists)
+    within = max(D[0, 1], D[2, 3])
+    between = min(D[0, 2], D[0, 3], D[1, 2], D[1, 3])
+    assert between > within
