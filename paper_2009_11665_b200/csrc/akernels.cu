@@ -114,182 +114,218 @@ struct AStepArgs {
     int tpo;            // lanes per output in the eMA (power of 2, <= 32)
 };
 
-// GT threads per row group; R 16-B vectors per thread per pass; U neighbours in flight
-template <typename T, typename RT, int GT, int R, int U>
+// ---- stage 1 for one row: B(i,·) over T ⊂ [k]∖{c(i)} into sB (group-uniform) ----
+template <typename T, int GT, int R, int U>
+__device__ __forceinline__ void gather_row(const AStepArgs &A, int64_t i, int ci, T *sB, int t, int g,
+                                           uint64_t pol_last, uint64_t pol_first) {
+    constexpr int VN = Vec<T>::N;
+    constexpr int32_t kIdMask = (1 << kClassShift) - 1;
+    const int64_t nvec_p = A.ldp / VN;
+    const size_t row_bytes = (size_t)A.ldp * sizeof(T);
+    const int k = A.k;
+    const int32_t *h = A.hcnt + (size_t)i * A.kp;
+    if (A.src_hist) {
+        for (int64_t y = t; y < A.cb; y += GT) sB[y] = (T)__ldg(h + y + (y >= ci ? 1 : 0));
+        return;
+    }
+    int64_t e = A.rowptr[i];
+    for (int x = 0; x < k; ++x) {
+        const int cnt = __ldg(h + x);
+        if (x != ci && cnt > 0) {
+            const int32_t *mp = A.pmap + ((size_t)x * k + ci) * A.cp;
+            for (int64_t v0 = 0; v0 < nvec_p; v0 += GT * R) {
+                uint4 acc[R];
+#pragma unroll
+                for (int q = 0; q < R; ++q) acc[q] = make_uint4(0, 0, 0, 0);
+                int64_t e2 = e;
+                const int64_t e3 = e + cnt;
+                for (; e2 + U <= e3; e2 += U) {
+                    int32_t jj[U];
+                    uint64_t pol[U];
+#pragma unroll
+                    for (int u = 0; u < U; ++u) {
+                        const int32_t b = __ldg(A.bcol + e2 + u);
+                        jj[u] = A.tagged ? (b & kIdMask) : b;
+                        pol[u] = (A.tagged && (b >> kClassShift) < A.hot_log2) ? pol_last : pol_first;
+                    }
+                    uint4 xv[U][R];
+#pragma unroll
+                    for (int u = 0; u < U; ++u)
+#pragma unroll
+                        for (int q = 0; q < R; ++q) {
+                            const int64_t v = v0 + q * GT + t;
+                            const char *src = A.mp + (size_t)jj[u] * row_bytes + v * 16;
+                            xv[u][q] = (v < nvec_p) ? (A.hint ? ldg16_pol(src, pol[u]) : ldg16(src))
+                                                    : make_uint4(0, 0, 0, 0);
+                        }
+#pragma unroll
+                    for (int u = 0; u < U; ++u)
+#pragma unroll
+                        for (int q = 0; q < R; ++q) Vec<T>::add(acc[q], xv[u][q]);
+                }
+                for (; e2 < e3; ++e2) {
+                    const int32_t b1 = __ldg(A.bcol + e2);
+                    const int32_t j1 = A.tagged ? (b1 & kIdMask) : b1;
+#pragma unroll
+                    for (int q = 0; q < R; ++q) {
+                        const int64_t v = v0 + q * GT + t;
+                        if (v < nvec_p) Vec<T>::add(acc[q], ldg16(A.mp + (size_t)j1 * row_bytes + v * 16));
+                    }
+                }
+                // push R_x into B: distinct targets within one colour
+#pragma unroll
+                for (int q = 0; q < R; ++q) {
+                    const int64_t v = v0 + q * GT + t;
+                    if (v < nvec_p) {
+#pragma unroll
+                        for (int el = 0; el < VN; ++el) {
+                            const int64_t u = v * VN + el;
+                            if (u < A.cp) {
+                                const int32_t tt = __ldg(mp + u);
+                                if (tt >= 0) sB[tt] += vget<T>(acc[q], el);
+                            }
+                        }
+                    }
+                }
+            }
+            group_sync<GT>(g);  // colours x and x' may push to the same T
+        }
+        e += cnt;
+    }
+}
+
+// GT threads per row group; R 16-B vectors per thread per pass; U neighbours in
+// flight; V rows per group per slot (V > 1 only for GENERAL non-top steps: each
+// split-table entry is loaded once and applied to V rows).
+template <typename T, typename RT, int GT, int R, int U, int V>
 __global__ void __launch_bounds__(256) astep_kernel(AStepArgs A) {
     constexpr int G = 256 / GT;
     constexpr int VN = Vec<T>::N;
     extern __shared__ __align__(16) unsigned char smem[];
     __shared__ RT red[8];
     const int g = threadIdx.x / GT, t = threadIdx.x % GT;
-    T *sB = reinterpret_cast<T *>(smem) + (size_t)g * A.smem_group;
-    T *sA = sB + A.ldb;
-    const int64_t nslots = (A.n + G - 1) / G;
-    const int64_t nvec_p = A.ldp / VN;
-    const size_t row_bytes = (size_t)A.ldp * sizeof(T);
-    const int k = A.k;
+    T *sBase = reinterpret_cast<T *>(smem) + (size_t)g * V * A.smem_group;
+    const int64_t per_slot = (int64_t)G * V;
+    const int64_t nslots = (A.n + per_slot - 1) / per_slot;
     const uint64_t pol_last = policy_evict_last(), pol_first = policy_evict_first();
-    constexpr int32_t kIdMask = (1 << kClassShift) - 1;
 
     for (int64_t slot = blockIdx.x; slot < nslots; slot += gridDim.x) {
-        const int64_t r = slot * G + g;
-        const bool act = r < A.n;
-        const int64_t i = act ? A.order[r] : 0;
-        const int ci = act ? (int)A.colors[i] : 0;
-        if (act) {
-            for (int64_t v = t; v < A.ldb / VN; v += GT) reinterpret_cast<uint4 *>(sB)[v] = make_uint4(0, 0, 0, 0);
-            if (A.comb == COMB_GENERAL && A.stage_a) {
-                const char *a = A.ma + (size_t)i * A.lda * sizeof(T);
-                for (int64_t v = t; v < A.lda / VN; v += GT) reinterpret_cast<uint4 *>(sA)[v] = ldg16(a + v * 16);
-            }
+        int64_t iv[V];
+        bool actv[V];
+#pragma unroll
+        for (int v = 0; v < V; ++v) {
+            const int64_t r = (slot * G + g) * V + v;
+            actv[v] = r < A.n;
+            iv[v] = actv[v] ? A.order[r] : 0;
         }
-        group_sync<GT>(g);
-        // ---- stage 1: B(i,·) over T ⊂ [k]∖{c(i)} ------------------------------
-        if (act) {
-            const int32_t *h = A.hcnt + (size_t)i * A.kp;
-            if (A.src_hist) {
-                for (int64_t y = t; y < A.cb; y += GT) sB[y] = (T)__ldg(h + y + (y >= ci ? 1 : 0));
-            } else {
-                int64_t e = A.rowptr[i];
-                for (int x = 0; x < k; ++x) {
-                    const int cnt = __ldg(h + x);
-                    if (x != ci && cnt > 0) {
-                        const int32_t *mp = A.pmap + ((size_t)x * k + ci) * A.cp;
-                        for (int64_t v0 = 0; v0 < nvec_p; v0 += GT * R) {
-                            uint4 acc[R];
+        // ---- stage 1: B rows (and staged M_a rows) into shared memory -----------
 #pragma unroll
-                            for (int q = 0; q < R; ++q) acc[q] = make_uint4(0, 0, 0, 0);
-                            int64_t e2 = e;
-                            const int64_t e3 = e + cnt;
-                            for (; e2 + U <= e3; e2 += U) {
-                                int32_t jj[U];
-                                uint64_t pol[U];
-#pragma unroll
-                                for (int u = 0; u < U; ++u) {
-                                    const int32_t b = __ldg(A.bcol + e2 + u);
-                                    jj[u] = A.tagged ? (b & kIdMask) : b;
-                                    pol[u] = (A.tagged && (b >> kClassShift) < A.hot_log2) ? pol_last : pol_first;
-                                }
-                                uint4 xv[U][R];
-#pragma unroll
-                                for (int u = 0; u < U; ++u)
-#pragma unroll
-                                    for (int q = 0; q < R; ++q) {
-                                        const int64_t v = v0 + q * GT + t;
-                                        xv[u][q] = (v < nvec_p) ? (A.hint ? ldg16_pol(A.mp + (size_t)jj[u] * row_bytes + v * 16, pol[u]) : ldg16(A.mp + (size_t)jj[u] * row_bytes + v * 16))
-                                                                : make_uint4(0, 0, 0, 0);
-                                    }
-#pragma unroll
-                                for (int u = 0; u < U; ++u)
-#pragma unroll
-                                    for (int q = 0; q < R; ++q) Vec<T>::add(acc[q], xv[u][q]);
-                            }
-                            for (; e2 < e3; ++e2) {
-                                const int32_t b1 = __ldg(A.bcol + e2);
-                                const int32_t j1 = A.tagged ? (b1 & kIdMask) : b1;
-#pragma unroll
-                                for (int q = 0; q < R; ++q) {
-                                    const int64_t v = v0 + q * GT + t;
-                                    if (v < nvec_p) Vec<T>::add(acc[q], ldg16(A.mp + (size_t)j1 * row_bytes + v * 16));
-                                }
-                            }
-                            // push R_x into B: distinct targets within one colour
-#pragma unroll
-                            for (int q = 0; q < R; ++q) {
-                                const int64_t v = v0 + q * GT + t;
-                                if (v < nvec_p) {
-#pragma unroll
-                                    for (int el = 0; el < VN; ++el) {
-                                        const int64_t u = v * VN + el;
-                                        if (u < A.cp) {
-                                            const int32_t tt = __ldg(mp + u);
-                                            if (tt >= 0) sB[tt] += vget<T>(acc[q], el);
-                                        }
-                                    }
-                                }
-                            }
-                        }
-                        group_sync<GT>(g);  // colours x and x' may push to the same T
-                    }
-                    e += cnt;
+        for (int v = 0; v < V; ++v) {
+            T *sB = sBase + (size_t)v * A.smem_group;
+            T *sA = sB + A.ldb;
+            const int64_t i = iv[v];
+            if (actv[v]) {
+                for (int64_t q = t; q < A.ldb / VN; q += GT) reinterpret_cast<uint4 *>(sB)[q] = make_uint4(0, 0, 0, 0);
+                if (A.comb == COMB_GENERAL && A.stage_a) {
+                    const char *a = A.ma + (size_t)i * A.lda * sizeof(T);
+                    for (int64_t q = t; q < A.lda / VN; q += GT) reinterpret_cast<uint4 *>(sA)[q] = ldg16(a + q * 16);
                 }
             }
+            group_sync<GT>(g);
+            if (actv[v]) gather_row<T, GT, R, U>(A, i, (int)A.colors[i], sB, t, g, pol_last, pol_first);
         }
         group_sync<GT>(g);
         // ---- stage 2: eMA over the universe [k-1] ------------------------------
         RT racc = 0;
-        if (act) {
-            if (!A.top) {
-                T *out = reinterpret_cast<T *>(A.ms) + (size_t)i * A.lds;
-                if (A.comb == COMB_ACTIVE_LEAF) {
-                    // M_s(i,·) = B(i,·): |T_s| - 1 = |T_p| and the colour sets coincide
-                    for (int64_t v = t; v < A.lds / VN; v += GT)
-                        reinterpret_cast<uint4 *>(out)[v] = reinterpret_cast<const uint4 *>(sB)[v];
-                } else {
-                    // split table term-major: entry (w, o) at w*cs + o, so the lanes
-                    // (consecutive outputs o) read consecutive words.  With few outputs
-                    // (cs < GT) tpo consecutive lanes share an output and split its terms.
-                    const T *ga = reinterpret_cast<const T *>(A.ma) + (size_t)i * A.lda;
-                    const int tpo = A.tpo, cs = (int)A.cs, nt = (int)A.nterms, lds = (int)A.lds;
-                    const int l = t % tpo;
-                    for (int ob = 0; ob < lds; ob += GT / tpo) {
-                        const int o = ob + t / tpo;
-                        T acc = 0;
-                        if (o < cs) {
-                            if (A.packed) {
-                                const uint32_t *p = reinterpret_cast<const uint32_t *>(A.idx) + o;
-                                if (A.stage_a) {
+        if (!A.top && A.comb == COMB_ACTIVE_LEAF) {
+            // M_s(i,·) = B(i,·): |T_s| - 1 = |T_p| and the colour sets coincide
+#pragma unroll
+            for (int v = 0; v < V; ++v)
+                if (actv[v]) {
+                    T *out = reinterpret_cast<T *>(A.ms) + (size_t)iv[v] * A.lds;
+                    const T *sB = sBase + (size_t)v * A.smem_group;
+                    for (int64_t q = t; q < A.lds / VN; q += GT)
+                        reinterpret_cast<uint4 *>(out)[q] = reinterpret_cast<const uint4 *>(sB)[q];
+                }
+        } else if (!A.top) {
+            // split table term-major: entry (w, o) at w*cs + o, so the lanes (consecutive
+            // outputs o) read consecutive words; each entry serves the group's V rows.
+            // With few outputs (cs < GT) tpo consecutive lanes share an output.
+            const int tpo = A.tpo, cs = (int)A.cs, nt = (int)A.nterms, lds = (int)A.lds;
+            const int l = t % tpo;
+            for (int ob = 0; ob < lds; ob += GT / tpo) {
+                const int o = ob + t / tpo;
+                T acc[V];
+#pragma unroll
+                for (int v = 0; v < V; ++v) acc[v] = 0;
+                if (o < cs) {
+                    if (A.packed && A.stage_a) {
+                        const uint32_t *p = reinterpret_cast<const uint32_t *>(A.idx) + o;
 #pragma unroll 4
-                                    for (int w = l; w < nt; w += tpo) {
-                                        const uint32_t q = __ldg(p + w * cs);
-                                        acc += sA[q & 0xffffu] * sB[q >> 16];
-                                    }
-                                } else {
-#pragma unroll 4
-                                    for (int w = l; w < nt; w += tpo) {
-                                        const uint32_t q = __ldg(p + w * cs);
-                                        acc += __ldg(ga + (q & 0xffffu)) * sB[q >> 16];
-                                    }
-                                }
-                            } else {
-                                const int2 *p = reinterpret_cast<const int2 *>(A.idx) + o;
-                                for (int w = l; w < nt; w += tpo) {
-                                    const int2 q = __ldg(p + (size_t)w * cs);
-                                    const T av = A.stage_a ? sA[q.x] : __ldg(ga + q.x);
-                                    acc += av * sB[q.y];
-                                }
+                        for (int w = l; w < nt; w += tpo) {
+                            const uint32_t q = __ldg(p + w * cs);
+                            const uint32_t ia = q & 0xffffu, ib = q >> 16;
+#pragma unroll
+                            for (int v = 0; v < V; ++v) {
+                                const T *sB = sBase + (size_t)v * A.smem_group;
+                                acc[v] += sB[A.ldb + ia] * sB[ib];
                             }
                         }
-                        if (tpo > 1) {  // tpo <= 32 and GT >= 32: whole warps, uniform trip count
+                    } else {
+                        for (int w = l; w < nt; w += tpo) {
+                            int32_t ia, ib;
+                            if (A.packed) {
+                                const uint32_t q = __ldg(reinterpret_cast<const uint32_t *>(A.idx) + o + (size_t)w * cs);
+                                ia = (int32_t)(q & 0xffffu);
+                                ib = (int32_t)(q >> 16);
+                            } else {
+                                const int2 q = __ldg(reinterpret_cast<const int2 *>(A.idx) + o + (size_t)w * cs);
+                                ia = q.x;
+                                ib = q.y;
+                            }
 #pragma unroll
-                            for (int off = 16; off > 0; off >>= 1)
-                                if (off < tpo) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+                            for (int v = 0; v < V; ++v) {
+                                const T *sB = sBase + (size_t)v * A.smem_group;
+                                const T av = A.stage_a ? sB[A.ldb + ia]
+                                                       : __ldg(reinterpret_cast<const T *>(A.ma) + (size_t)iv[v] * A.lda + ia);
+                                acc[v] += av * sB[ib];
+                            }
                         }
-                        if (l == 0 && o < lds) out[o] = acc;
                     }
                 }
-            } else {
-                const T *ga = reinterpret_cast<const T *>(A.ma) + (size_t)i * A.lda;
+#pragma unroll
+                for (int v = 0; v < V; ++v) {
+                    if (tpo > 1) {  // tpo <= 32 and GT >= 32: whole warps, uniform trip count
+#pragma unroll
+                        for (int off = 16; off > 0; off >>= 1)
+                            if (off < tpo) acc[v] += __shfl_xor_sync(0xffffffffu, acc[v], off);
+                    }
+                    if (actv[v] && l == 0 && o < lds)
+                        reinterpret_cast<T *>(A.ms)[(size_t)iv[v] * A.lds + o] = acc[v];
+                }
+            }
+        } else if (actv[0]) {
+            // top (V == 1): colorful_i = Σ_{I_a} M_a(i,I_a)·B(i,[k-1]∖I_a)
+            const T *sB = sBase;
+            const T *ga = reinterpret_cast<const T *>(A.ma) + (size_t)iv[0] * A.lda;
+            for (int64_t w = t; w < A.nterms; w += GT) {
+                int32_t ia, ib;
                 if (A.packed) {
-                    const uint32_t *sp = reinterpret_cast<const uint32_t *>(A.idx);
-                    for (int64_t w = t; w < A.nterms; w += GT) {
-                        const uint32_t q = __ldg(sp + w);
-                        const T av = A.stage_a ? sA[q & 0xffffu] : __ldg(ga + (q & 0xffffu));
-                        racc += (RT)av * (RT)sB[q >> 16];
-                    }
+                    const uint32_t q = __ldg(reinterpret_cast<const uint32_t *>(A.idx) + w);
+                    ia = (int32_t)(q & 0xffffu);
+                    ib = (int32_t)(q >> 16);
                 } else {
-                    const int2 *sp = reinterpret_cast<const int2 *>(A.idx);
-                    for (int64_t w = t; w < A.nterms; w += GT) {
-                        const int2 q = __ldg(sp + w);
-                        const T av = A.stage_a ? sA[q.x] : __ldg(ga + q.x);
-                        racc += (RT)av * (RT)sB[q.y];
-                    }
+                    const int2 q = __ldg(reinterpret_cast<const int2 *>(A.idx) + w);
+                    ia = q.x;
+                    ib = q.y;
                 }
+                const T av = A.stage_a ? sB[A.ldb + ia] : __ldg(ga + ia);
+                racc += (RT)av * (RT)sB[ib];
             }
         }
         if (A.top) {
             RT s = group_reduce<RT, GT>(racc, g, red);
-            if (act && t == 0) reinterpret_cast<RT *>(A.rowval)[i] = s;
+            if (actv[0] && t == 0) reinterpret_cast<RT *>(A.rowval)[iv[0]] = s;
         }
         group_sync<GT>(g);
     }
@@ -341,11 +377,11 @@ int launch_bucket(const Graph &g, const Plan &pl, const uint8_t *colors, int32_t
     return (int)cudaGetLastError();
 }
 
-template <typename T, typename RT, int GT, int R, int U>
+template <typename T, typename RT, int GT, int R, int U, int V = 1>
 static int launch_astep_t(const AStepArgs &A, void *stream) {
-    auto kern = astep_kernel<T, RT, GT, R, U>;
+    auto kern = astep_kernel<T, RT, GT, R, U, V>;
     constexpr int G = 256 / GT;
-    size_t smem = (size_t)G * A.smem_group * sizeof(T);
+    size_t smem = (size_t)G * V * A.smem_group * sizeof(T);
     if (smem > 227 * 1024) return -1;
     static size_t configured = 0;
     if (smem > 48 * 1024 && smem > configured) {
@@ -356,7 +392,7 @@ static int launch_astep_t(const AStepArgs &A, void *stream) {
     int occ = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 256, smem);
     if (occ < 1) occ = 1;
-    int64_t nslots = (A.n + G - 1) / G;
+    int64_t nslots = (A.n + (int64_t)G * V - 1) / ((int64_t)G * V);
     int64_t blocks = std::min<int64_t>(nslots, (int64_t)occ * num_sms());
     if (blocks < 1) blocks = 1;
     kern<<<(unsigned)blocks, 256, smem, (cudaStream_t)stream>>>(A);
@@ -384,7 +420,7 @@ template <typename T, typename RT>
 static int launch_astep_cfg(const AStepArgs &A0, void *stream) {
     AStepArgs A = A0;
     constexpr int VN = Vec<T>::N;
-    static int tune = -1;  // SG2V_TUNE (experiments only): 1 narrow U=16; 2 wide R=2/U=8; 4 wide R=4/U=4
+    static int tune = -1;  // SG2V_TUNE (experiments only): 1 narrow U=16; 2 wide R=2/U=8; 4 wide R=4/U=4; 5 no V-rows
     if (tune < 0) {
         const char *e = getenv("SG2V_TUNE");
         tune = e ? atoi(e) : 0;
@@ -399,6 +435,18 @@ static int launch_astep_cfg(const AStepArgs &A0, void *stream) {
     A.tpo = 1;
     if (A.comb == COMB_GENERAL && !A.top && gt >= 32)
         while (A.tpo < 32 && A.cs * A.tpo * 2 <= gt) A.tpo *= 2;
+    // eMA-heavy GENERAL steps: V = 4 rows share every split-table load
+    const bool multi = A.comb == COMB_GENERAL && !A.top && A.nterms >= 8 && gt >= 32 && tune != 5 &&
+                       (size_t)(256 / gt) * 4 * A.smem_group * sizeof(T) <= 200 * 1024;
+    if (multi) {
+        if (nvec > 256) return launch_astep_t<T, RT, 256, 1, 16, 4>(A, stream);
+        switch (gt) {
+            case 32: return launch_astep_t<T, RT, 32, 1, 8, 4>(A, stream);
+            case 64: return launch_astep_t<T, RT, 64, 1, 8, 4>(A, stream);
+            case 128: return launch_astep_t<T, RT, 128, 1, 8, 4>(A, stream);
+            default: return launch_astep_t<T, RT, 256, 1, 8, 4>(A, stream);
+        }
+    }
     if (nvec > 256) {
         if (tune == 2) return launch_astep_t<T, RT, 256, 2, 8>(A, stream);
         if (tune == 4) return launch_astep_t<T, RT, 256, 4, 4>(A, stream);
