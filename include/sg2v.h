@@ -100,15 +100,15 @@ typedef struct {
     int64_t iter_offset;      /* colouring index of the first colouring (default 0) */
     int64_t iter_stride;      /* colouring t of the call is j = iter_offset +
                                  t*iter_stride (default 1; replica sharding)        */
-    int32_t mode;             /* 0 = replicas (only mode implemented)                */
-    void *nccl_comm;          /* reserved (vertex-partitioned mode), must be NULL    */
+    int32_t mode;             /* 0 = replicas / single GPU, 1 = vertex partition       */
+    void *nccl_comm;          /* mode 1: the sg2v_comm of this rank                  */
     int32_t device;           /* CUDA ordinal; -1 = current device                   */
     uint64_t mem_budget_bytes;/* planning budget: the planner picks the fastest plan
                                  whose workspace fits; 0 = device memory minus 6 GiB
                                  (unlimited for host-only planning).  sg2v_count also
                                  refuses (ENOMEM) a library-allocated workspace larger
                                  than the free device memory                         */
-    int32_t col_tile;         /* reserved, 0                                         */
+    int32_t col_tile;         /* mode 1: column tile width in elements (0 = auto)    */
     void *stream;             /* cudaStream_t (e.g. torch's current stream); NULL =
                                  legacy default stream                               */
     void *workspace;          /* caller-owned device buffer (>= sg2v_workspace_bytes)
@@ -176,6 +176,35 @@ sg2v_status sg2v_count_batch(const sg2v_graph *g, const sg2v_template *const *te
 /* Workspace bytes of sg2v_count_batch (thread-local layout / budget options). */
 sg2v_status sg2v_workspace_bytes_batch(const sg2v_graph *g, const sg2v_template *const *templates,
                                        int32_t m, sg2v_precision precision, uint64_t *bytes);
+
+/*
+ * Vertex-partitioned mode (SURVEY §8(e) "V": capacity for tables larger than one
+ * GPU).  Rank r of W owns rows [r*nl, r*nl + n_local) of G and of every count
+ * table, nl = ceil(n_global / W).  Each SpMM step all-gathers the passive table
+ * in column tiles (options.col_tile elements; 0 = ~512 MB staging) and every rank
+ * pushes its own rows' colour-bucket sums; the eMA and the top step are row-local;
+ * the per-rank Σ_i are all-gathered and summed in rank order.  Select it with
+ * options.mode = 1 and options.nccl_comm = an sg2v_comm (anchored layout, one
+ * template per call).  Values equal the single-GPU ones (exact in U64).
+ */
+typedef struct sg2v_comm sg2v_comm;
+/* host all-gather: recv[r*bytes .. (r+1)*bytes) = rank r's send (returns 0 on success) */
+typedef int32_t (*sg2v_allgather_fn)(const void *send, void *recv, uint64_t bytes, void *user);
+/* NCCL transport (one process per GPU): rank 0 creates the id, the caller
+ * broadcasts its 128 bytes (e.g. torch.distributed), every rank calls init. */
+sg2v_status sg2v_comm_unique_id(uint8_t id_out[128]);
+sg2v_status sg2v_comm_init_nccl(const uint8_t id[128], int32_t rank, int32_t world, sg2v_comm **out);
+/* Host-callback transport (tests: gloo, several processes on one GPU). */
+sg2v_status sg2v_comm_init_callback(int32_t rank, int32_t world, sg2v_allgather_fn fn, void *user,
+                                    sg2v_comm **out);
+void sg2v_comm_free(sg2v_comm *c);
+/* Rows [row_begin, row_begin + n_local) of an n_global-vertex graph: row_offsets
+ * int64[n_local+1] starting at 0, col_indices int32[nnz] GLOBAL ids (sorted per
+ * row, no self-loops, symmetric as a whole graph).  Host or device pointers as in
+ * sg2v_graph_load_csr (VALIDATE is not available per partition). */
+sg2v_status sg2v_graph_load_partition(int64_t n_global, int64_t row_begin, int64_t n_local,
+                                      const int64_t *row_offsets, const int32_t *col_indices,
+                                      int64_t nnz, uint32_t flags, sg2v_graph **out);
 
 /*
  * sg2v_colorize — kernel a1 alone: writes

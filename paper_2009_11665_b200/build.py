@@ -40,7 +40,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     cuda_lib = "/usr/local/cuda/lib64"
     cmd = [nvcc(), "-O3", "-std=c++17", "-shared", "-Xcompiler", "-fPIC,-O3",
            "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo",
-           "-cudart", "shared", "-Xlinker", f"-rpath,{cuda_lib}",
+           "-cudart", "shared", "-Xlinker", f"-rpath,{cuda_lib}", "-ldl",
            "-I", os.path.join(ROOT, "include"),
            "-o", LIB] + [os.path.join(CSRC, s) for s in SOURCES]
     if verbose:

@@ -42,8 +42,10 @@ __global__ void __launch_bounds__(256) bucket_kernel(int64_t n, int k, int kp, c
                                                      const int32_t *__restrict__ col,
                                                      const uint8_t *__restrict__ colors,
                                                      const uint8_t *__restrict__ vclass,
-                                                     int32_t *__restrict__ hcnt, int32_t *__restrict__ bcol) {
-    const bool tag = n < (int64_t(1) << kClassShift);
+                                                     int32_t *__restrict__ hcnt, int32_t *__restrict__ bcol,
+                                                     int64_t row_begin) {
+    // rows are local (row_begin + i is the global id); neighbour ids are global
+    const bool tag = vclass != nullptr && n < (int64_t(1) << kClassShift);
     const int lane = threadIdx.x & 31;
     const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
     for (int64_t i = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); i < n; i += warps) {
@@ -112,6 +114,12 @@ struct AStepArgs {
     int packed;         // split pairs packed as ia | ip << 16 (both < 2^16)
     int stage_a;        // M_a row staged in shared memory (else read through L1)
     int tpo;            // lanes per output in the eMA (power of 2, <= 32)
+    // vertex-partitioned mode: B rows live in global memory
+    int64_t cp_map;     // row length of the push map (= cp unless tiled)
+    int64_t u0;         // first passive column of this tile (push-map offset)
+    int tile_mode;      // stage 1 only: gather a staged column tile, push into bg rows
+    int bsrc_global;    // stage 1 = copy the completed B row from bg
+    char *bg;           // [n_local][ldb] B rows (tile_mode / bsrc_global)
 };
 
 // ---- stage 1 for one row: B(i,·) over T ⊂ [k]∖{c(i)} into sB (group-uniform) ----
@@ -132,7 +140,7 @@ __device__ __forceinline__ void gather_row(const AStepArgs &A, int64_t i, int ci
     for (int x = 0; x < k; ++x) {
         const int cnt = __ldg(h + x);
         if (x != ci && cnt > 0) {
-            const int32_t *mp = A.pmap + ((size_t)x * k + ci) * A.cp;
+            const int32_t *mp = A.pmap + ((size_t)x * k + ci) * A.cp_map + A.u0;
             for (int64_t v0 = 0; v0 < nvec_p; v0 += GT * R) {
                 uint4 acc[R];
 #pragma unroll
@@ -224,15 +232,31 @@ __global__ void __launch_bounds__(256) astep_kernel(AStepArgs A) {
             T *sB = sBase + (size_t)v * A.smem_group;
             T *sA = sB + A.ldb;
             const int64_t i = iv[v];
+            if (A.tile_mode) {
+                // vertex-partitioned: push this column tile's R_x sums into the row's
+                // B in global memory (zeroed before the first tile)
+                T *gB = reinterpret_cast<T *>(A.bg) + (size_t)i * A.ldb;
+                if (actv[v]) gather_row<T, GT, R, U>(A, i, (int)A.colors[i], gB, t, g, pol_last, pol_first);
+                continue;
+            }
             if (actv[v]) {
-                for (int64_t q = t; q < A.ldb / VN; q += GT) reinterpret_cast<uint4 *>(sB)[q] = make_uint4(0, 0, 0, 0);
+                if (A.bsrc_global) {
+                    const char *b = A.bg + (size_t)i * A.ldb * sizeof(T);
+                    for (int64_t q = t; q < A.ldb / VN; q += GT) reinterpret_cast<uint4 *>(sB)[q] = ldg16(b + q * 16);
+                } else {
+                    for (int64_t q = t; q < A.ldb / VN; q += GT) reinterpret_cast<uint4 *>(sB)[q] = make_uint4(0, 0, 0, 0);
+                }
                 if (A.comb == COMB_GENERAL && A.stage_a) {
                     const char *a = A.ma + (size_t)i * A.lda * sizeof(T);
                     for (int64_t q = t; q < A.lda / VN; q += GT) reinterpret_cast<uint4 *>(sA)[q] = ldg16(a + q * 16);
                 }
             }
             group_sync<GT>(g);
-            if (actv[v]) gather_row<T, GT, R, U>(A, i, (int)A.colors[i], sB, t, g, pol_last, pol_first);
+            if (actv[v] && !A.bsrc_global) gather_row<T, GT, R, U>(A, i, (int)A.colors[i], sB, t, g, pol_last, pol_first);
+        }
+        if (A.tile_mode) {
+            group_sync<GT>(g);
+            continue;
         }
         group_sync<GT>(g);
         // ---- stage 2: eMA over the universe [k-1] ------------------------------
@@ -371,8 +395,9 @@ int launch_bucket(const Graph &g, const Plan &pl, const uint8_t *colors, int32_t
     int64_t blocks = std::min<int64_t>((g.n + 7) / 8, (int64_t)num_sms() * 8);
     double bytes = g.nnz * 9.0 + g.nnz * 4.0 + g.n * 16.0 + (double)g.n * pl.kp * 4.0;
     prof_begin(1, stream);
-    bucket_kernel<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(g.n, pl.k, (int)pl.kp, g.d_rowptr, g.d_col,
-                                                                      colors, g.d_vclass, hcnt, bcol);
+    bucket_kernel<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(
+        g.n, pl.k, (int)pl.kp, g.d_rowptr, g.d_col, colors, g.partitioned ? nullptr : g.d_vclass, hcnt, bcol,
+        g.row_begin);
     prof_end(1, bytes, stream);
     return (int)cudaGetLastError();
 }
@@ -458,10 +483,15 @@ static int launch_astep_cfg(const AStepArgs &A0, void *stream) {
 
 int launch_astep(const Graph &g, const Plan &pl, const Step &st, const uint8_t *colors, const int32_t *hcnt,
                  const int32_t *bcol, char *tables, void *rowval, void *stream) {
+    return launch_astep_vp(g, pl, st, colors, hcnt, bcol, tables, rowval, stream, nullptr);
+}
+
+int launch_astep_vp(const Graph &g, const Plan &pl, const Step &st, const uint8_t *colors, const int32_t *hcnt,
+                    const int32_t *bcol, char *tables, void *rowval, void *stream, const VpArgs *vp) {
     if (g.n <= 0) return 0;
     const int32_t *idx = pl.d_index + st.idx_off;
-    const char *src = (st.src == SRC_HIST) ? nullptr : tables + pl.bufs[st.buf_p].offset;
-    if (st.top && st.comb == COMB_ACTIVE_LEAF) {
+    const char *src = (st.src == SRC_HIST || (vp && vp->mode == 2)) ? nullptr : tables + pl.bufs[st.buf_p].offset;
+    if (st.top && st.comb == COMB_ACTIVE_LEAF && !vp) {
         int64_t blocks = std::min<int64_t>((g.n + 7) / 8, (int64_t)num_sms() * 8);
         int srch = st.src == SRC_HIST;
         prof_begin(3, stream);
@@ -507,6 +537,11 @@ int launch_astep(const Graph &g, const Plan &pl, const Step &st, const uint8_t *
     A.nterms = st.nterms;
     A.rowval = rowval;
     A.packed = st.packed;
+    A.cp_map = st.cp;
+    A.u0 = 0;
+    A.tile_mode = 0;
+    A.bsrc_global = 0;
+    A.bg = nullptr;
     // stage M_a next to B only while both fit comfortably (occupancy); else L1
     A.stage_a = (st.comb == COMB_GENERAL) && (st.ldb + st.lda) * pl.elem <= 100 * 1024;
     A.tpo = 1;  // set per launch configuration (launch_astep_cfg)
@@ -529,14 +564,69 @@ int launch_astep(const Graph &g, const Plan &pl, const Step &st, const uint8_t *
         if (hint < 0) { const char *e = getenv("SG2V_HINT"); hint = e ? atoi(e) : 1; }
         A.hint = hint;
     }
+    A.tagged = A.tagged && g.d_vclass != nullptr && !g.partitioned;
+    if (vp && vp->mode == 1) {  // column tile of the all-gathered passive table -> bg
+        A.mp = vp->stage;
+        A.ldp = vp->stage_ld;
+        A.cp = vp->cnt;
+        A.u0 = vp->u0;
+        A.tile_mode = 1;
+        A.bg = vp->bg;
+        A.smem_group = 0;
+        A.stage_a = 0;
+        A.hint = 0;
+    } else if (vp && vp->mode == 2) {  // combine: B rows complete in bg
+        A.bsrc_global = 1;
+        A.bg = vp->bg;
+        A.src_hist = 0;
+    }
     int cls = st.top ? 3 : 2;
     prof_begin(cls, stream);
     int rc;
     if (pl.prec == SG2V_F32) rc = launch_astep_cfg<float, double>(A, stream);
     else if (pl.prec == SG2V_F64) rc = launch_astep_cfg<double, double>(A, stream);
     else rc = launch_astep_cfg<u64, u64>(A, stream);
-    prof_end(cls, st.alg_bytes, stream);
+    prof_end(cls, vp ? 0.0 : st.alg_bytes, stream);
     return rc;
+}
+
+// ---------------------------------------------------------------------------
+// vertex-partitioned mode helpers
+// ---------------------------------------------------------------------------
+// dst[i][0..w) = src[i][u0..u0+w) (16-B vectors; row strides ldv / dstv vectors)
+__global__ void pack_tile_kernel(int64_t n, const uint4 *__restrict__ src, int64_t ldv, int64_t u0v, int64_t wv,
+                                 uint4 *__restrict__ dst, int64_t dstv) {
+    const int64_t total = n * wv;
+    for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < total; q += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i = q / wv, v = q - i * wv;
+        dst[i * dstv + v] = src[i * ldv + u0v + v];
+    }
+}
+
+int launch_pack_tile(int64_t n, const char *src, int64_t ld_bytes, int64_t u0_bytes, int64_t w_bytes, char *dst,
+                     int64_t dst_ld_bytes, void *stream) {
+    if (n <= 0 || w_bytes <= 0) return 0;
+    const int64_t total = n * (w_bytes / 16);
+    const int64_t blocks = std::min<int64_t>((total + 255) / 256, (int64_t)num_sms() * 16);
+    pack_tile_kernel<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(
+        n, (const uint4 *)src, ld_bytes / 16, u0_bytes / 16, w_bytes / 16, (uint4 *)dst, dst_ld_bytes / 16);
+    return (int)cudaGetLastError();
+}
+
+template <typename T, typename RT>
+__global__ void bg_rowval_kernel(int64_t n, const T *__restrict__ bg, int64_t ldb, RT *__restrict__ rowval) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        rowval[i] = (RT)bg[i * ldb];
+}
+
+int launch_bg_rowval(const Plan &pl, int64_t n, const char *bg, int64_t ldb, void *rowval, void *stream) {
+    if (n <= 0) return 0;
+    const int64_t blocks = std::min<int64_t>((n + 255) / 256, (int64_t)num_sms() * 16);
+    cudaStream_t s = (cudaStream_t)stream;
+    if (pl.prec == SG2V_F32) bg_rowval_kernel<float, double><<<(unsigned)blocks, 256, 0, s>>>(n, (const float *)bg, ldb, (double *)rowval);
+    else if (pl.prec == SG2V_F64) bg_rowval_kernel<double, double><<<(unsigned)blocks, 256, 0, s>>>(n, (const double *)bg, ldb, (double *)rowval);
+    else bg_rowval_kernel<u64, u64><<<(unsigned)blocks, 256, 0, s>>>(n, (const u64 *)bg, ldb, (u64 *)rowval);
+    return (int)cudaGetLastError();
 }
 
 }  // namespace sg2v

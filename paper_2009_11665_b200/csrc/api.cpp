@@ -9,7 +9,51 @@
 #include <string>
 #include <vector>
 
+#include <dlfcn.h>
+#include <nccl.h>
+
 #include "sg2v_internal.h"
+
+// NCCL is resolved at first use (dlopen, preferring the copy torch already loaded)
+// instead of at link time: linking the system libnccl.so.2 would shadow torch's
+// newer one for any process that loads libsg2v.so first.
+namespace {
+struct NcclApi {
+    bool ok = false;
+    ncclResult_t (*getUniqueId)(ncclUniqueId *) = nullptr;
+    ncclResult_t (*commInitRank)(ncclComm_t *, int, ncclUniqueId, int) = nullptr;
+    ncclResult_t (*allGather)(const void *, void *, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*commDestroy)(ncclComm_t) = nullptr;
+    const char *(*getErrorString)(ncclResult_t) = nullptr;
+};
+const NcclApi &nccl_api() {
+    static NcclApi api;
+    static bool tried = false;
+    if (tried) return api;
+    tried = true;
+    void *h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+    if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) return api;
+    api.getUniqueId = (decltype(api.getUniqueId))dlsym(h, "ncclGetUniqueId");
+    api.commInitRank = (decltype(api.commInitRank))dlsym(h, "ncclCommInitRank");
+    api.allGather = (decltype(api.allGather))dlsym(h, "ncclAllGather");
+    api.commDestroy = (decltype(api.commDestroy))dlsym(h, "ncclCommDestroy");
+    api.getErrorString = (decltype(api.getErrorString))dlsym(h, "ncclGetErrorString");
+    api.ok = api.getUniqueId && api.commInitRank && api.allGather && api.commDestroy && api.getErrorString;
+    return api;
+}
+}  // namespace
+
+// Communicator of the vertex-partitioned mode: NCCL over NVLink (one process per
+// GPU), or a host all-gather callback (tests: gloo, several processes per GPU).
+struct sg2v_comm {
+    int rank = 0, world = 1;
+    ncclComm_t nccl = nullptr;
+    sg2v_allgather_fn cb = nullptr;
+    void *user = nullptr;
+    char *hsend = nullptr, *hrecv = nullptr;  // pinned staging of the callback transport
+    size_t hcap = 0;
+};
 
 namespace sg2v {
 
@@ -181,7 +225,7 @@ void sg2v_options_default(sg2v_options *o) {
 
 sg2v_status sg2v_set_options(const sg2v_options *o) {
     if (!o) { set_error("options is NULL"); return SG2V_EINVAL; }
-    if (o->mode != 0 || o->nccl_comm) { set_error("only mode 0 (replicas) is implemented"); return SG2V_EINVAL; }
+    if (o->mode < 0 || o->mode > 1) { set_error("mode must be 0 (replicas) or 1 (vertex partition)"); return SG2V_EINVAL; }
     g_opts = *o;
     g_opts_init = true;
     return SG2V_OK;
@@ -385,6 +429,191 @@ static sg2v_status batch_plans(const sg2v_graph *g, const sg2v_template *const *
     return SG2V_OK;
 }
 
+// ----------------------------------------------------------- vertex partition
+static sg2v_status comm_allgather(sg2v_comm *c, const void *send, void *recv, size_t bytes, cudaStream_t s) {
+    if (c->nccl) {
+        ncclResult_t r = nccl_api().allGather(send, recv, bytes, ncclUint8, c->nccl, s);
+        if (r != ncclSuccess) {
+            set_error(std::string("ncclAllGather: ") + nccl_api().getErrorString(r));
+            return SG2V_ENCCL;
+        }
+        return SG2V_OK;
+    }
+    if (!c->cb) { set_error("communicator has no transport"); return SG2V_EINVAL; }
+    const size_t need = bytes * (size_t)c->world;
+    if (c->hcap < need) {
+        if (c->hsend) cudaFreeHost(c->hsend);
+        if (c->hrecv) cudaFreeHost(c->hrecv);
+        SG2V_CK(cudaMallocHost((void **)&c->hsend, std::max<size_t>(bytes, 1)));
+        SG2V_CK(cudaMallocHost((void **)&c->hrecv, std::max<size_t>(need, 1)));
+        c->hcap = need;
+    }
+    SG2V_CK(cudaMemcpyAsync(c->hsend, send, bytes, cudaMemcpyDeviceToHost, s));
+    SG2V_CK(cudaStreamSynchronize(s));
+    if (c->cb(c->hsend, c->hrecv, (uint64_t)bytes, c->user) != 0) {
+        set_error("all-gather callback failed");
+        return SG2V_ENCCL;
+    }
+    SG2V_CK(cudaMemcpyAsync(recv, c->hrecv, need, cudaMemcpyHostToDevice, s));
+    return SG2V_OK;
+}
+
+// 1D vertex partition: rank r owns rows [r·nl, r·nl + n_local) of
+// every table (nl = ceil(n_global / world)); per gather step the passive table is
+// all-gathered column tile by column tile into [world·nl][tile_w] staging and each
+// rank pushes its own rows' colour-bucket sums into B rows in global memory; the
+// eMA / top then run on the local rows, and the per-rank Σ_i are all-gathered.
+static sg2v_status count_vp(const sg2v_graph *g, const sg2v_template *t, int32_t k, int64_t n_iter, uint64_t seed,
+                            sg2v_options o, double *estimate, double *colorful_out, uint64_t *colorful_u64_out) {
+    sg2v_comm *c = (sg2v_comm *)o.nccl_comm;
+    if (!c) { set_error("mode 1 needs options.nccl_comm (sg2v_comm_init_*)"); return SG2V_EINVAL; }
+    if (o.layout != 0) { set_error("the vertex-partitioned mode uses the anchored layout"); return SG2V_EINVAL; }
+    const int64_t n_global = g->partitioned ? g->n_global : g->n;
+    const int64_t nl = (n_global + c->world - 1) / c->world;
+    const int64_t begin = g->partitioned ? g->row_begin : 0;
+    if (begin != (int64_t)c->rank * nl || g->n != std::max<int64_t>(0, std::min(nl, n_global - begin))) {
+        set_error("partition must be rows [rank*nl, rank*nl + n_local) with nl = ceil(n_global/world)");
+        return SG2V_EINVAL;
+    }
+    const int dev = g->device;
+    int prev_dev = 0;
+    cudaGetDevice(&prev_dev);
+    sg2v_status st = ensure_device(dev);
+    if (st != SG2V_OK) return st;
+    struct Restore { int d; ~Restore() { cudaSetDevice(d); } } restore{prev_dev};
+    const bool u64mode = o.precision == SG2V_U64;
+    cudaStream_t s = (cudaStream_t)o.stream;
+    std::vector<double> resf(n_iter, 0.0);
+    std::vector<uint64_t> resu(n_iter, 0);
+    if (k == 1) {
+        for (int64_t q = 0; q < n_iter; ++q) { resf[q] = (double)n_global; resu[q] = (uint64_t)n_global; }
+    } else {
+        // plan on the local rows; staging sized for world·nl global rows
+        auto key = std::make_tuple((int)o.precision, g->n, g->nnz, -(g->device + 1) - 1000 * c->world, 0,
+                                   (uint64_t)o.col_tile);
+        auto &slot = const_cast<Template &>(*(const Template *)t).plans[key];
+        if (!slot) {
+            std::unique_ptr<Plan> pl;
+            st = make_plan(*t, std::max<int64_t>(g->n, 1), std::max<int64_t>(g->nnz, 1), o.precision, LAYOUT_ANCHORED,
+                           0, pl, (int64_t)c->world * nl, o.col_tile);
+            if (st != SG2V_OK) return st;
+            slot = std::move(pl);
+        }
+        Plan *pl = slot.get();
+        if (!pl->d_index) {
+            SG2V_CK(cudaMalloc(&pl->d_index, pl->index.size() * sizeof(int32_t)));
+            SG2V_CK(cudaMemcpy(pl->d_index, pl->index.data(), pl->index.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
+        }
+        char *ws = (char *)o.workspace;
+        bool own = false;
+        if (ws) {
+            if (o.workspace_bytes < (uint64_t)pl->ws_bytes) {
+                set_error("workspace too small: need " + std::to_string(pl->ws_bytes) + " bytes");
+                return SG2V_ENOMEM;
+            }
+        } else {
+            keep_pool(dev);
+            SG2V_CK(cudaMallocAsync((void **)&ws, pl->ws_bytes, s));
+            own = true;
+        }
+        struct Free { char *p; bool own; cudaStream_t s; ~Free() { if (own) cudaFreeAsync(p, s); } } freer{ws, own, s};
+        uint8_t *colors_g = (uint8_t *)(ws + pl->off_colors_g);
+        uint8_t *colors_l = colors_g + begin;
+        int32_t *hcnt = (int32_t *)(ws + pl->off_hcnt);
+        int32_t *bcol = (int32_t *)(ws + pl->off_bcol);
+        void *rowval = ws + pl->off_rowval;
+        void *partial = ws + pl->off_partial;
+        char *part = ws + pl->off_part;  // [0]: this rank's Σ_i, [8..]: all ranks'
+        const int64_t E = pl->elem, W = pl->tile_w;
+        const int vn = 16 / pl->elem;
+        std::vector<uint64_t> hpart(c->world);
+        for (int64_t q = 0; q < n_iter; ++q) {
+            const int64_t j = o.iter_offset + q * o.iter_stride;
+            int rc = launch_colorize(seed, j, n_global, k, colors_g, s);  // every rank colours every vertex
+            if (rc) return cuda_fail("colorize", rc);
+            if (g->n > 0 && (rc = launch_bucket(*g, *pl, colors_g, hcnt, bcol, s))) return cuda_fail("bucket", rc);
+            int par = 0;
+            for (const Step &stp : pl->steps) {
+                if (stp.src == SRC_HIST) {  // local (the histogram is local)
+                    rc = launch_astep_vp(*g, *pl, stp, colors_l, hcnt, bcol, ws, rowval, s, nullptr);
+                    if (rc) return cuda_fail("step", rc == -1 ? 0 : rc);
+                    continue;
+                }
+                const bool bg_is_out = !stp.top && stp.comb == COMB_ACTIVE_LEAF;
+                char *bg = bg_is_out ? ws + pl->bufs[stp.buf_out].offset : ws + pl->off_bg;
+                SG2V_CK(cudaMemsetAsync(bg, 0, (size_t)std::max<int64_t>(g->n, 1) * stp.ldb * E, s));
+                const char *mp = ws + pl->bufs[stp.buf_p].offset;
+                for (int64_t u0 = 0; u0 < stp.cp; u0 += W) {
+                    const int64_t cnt = std::min<int64_t>(W, stp.cp - u0);
+                    const int64_t wb = ((cnt + vn - 1) / vn) * vn * E;
+                    char *send = ws + pl->off_send + (size_t)par * nl * W * E;
+                    char *stage = ws + pl->off_stage + (size_t)par * c->world * nl * W * E;
+                    if (g->n > 0 && (rc = launch_pack_tile(g->n, mp, stp.ldp * E, u0 * E, wb, send, W * E, s)))
+                        return cuda_fail("pack", rc);
+                    st = comm_allgather(c, send, stage, (size_t)nl * W * E, s);
+                    if (st != SG2V_OK) return st;
+                    VpArgs va;
+                    va.mode = 1;
+                    va.stage = stage;
+                    va.stage_ld = W;
+                    va.u0 = u0;
+                    va.cnt = cnt;
+                    va.bg = bg;
+                    rc = launch_astep_vp(*g, *pl, stp, colors_l, hcnt, bcol, ws, rowval, s, &va);
+                    if (rc) return cuda_fail("tile", rc == -1 ? 0 : rc);
+                    par ^= 1;
+                }
+                if (bg_is_out) continue;
+                if (stp.top && stp.comb == COMB_ACTIVE_LEAF) {
+                    rc = launch_bg_rowval(*pl, g->n, bg, stp.ldb, rowval, s);
+                } else {
+                    VpArgs va;
+                    va.mode = 2;
+                    va.bg = bg;
+                    rc = launch_astep_vp(*g, *pl, stp, colors_l, hcnt, bcol, ws, rowval, s, &va);
+                }
+                if (rc) return cuda_fail("combine", rc == -1 ? 0 : rc);
+            }
+            if (g->n > 0) {
+                rc = launch_reduce(*pl, g->n, rowval, partial, part, s);
+                if (rc) return cuda_fail("reduce", rc);
+            } else {
+                SG2V_CK(cudaMemsetAsync(part, 0, 8, s));
+            }
+            st = comm_allgather(c, part, part + 8, 8, s);
+            if (st != SG2V_OK) return st;
+            SG2V_CK(cudaMemcpyAsync(hpart.data(), part + 8, 8 * c->world, cudaMemcpyDeviceToHost, s));
+            SG2V_CK(cudaStreamSynchronize(s));
+            uint64_t su = 0;
+            double sf = 0.0;
+            for (int r = 0; r < c->world; ++r) {  // rank order: deterministic
+                double f;
+                std::memcpy(&f, &hpart[r], 8);
+                su += hpart[r];
+                sf += f;
+            }
+            resu[q] = su;
+            resf[q] = sf;
+        }
+    }
+    bool finite = true;
+    double sum = 0.0;
+    for (int64_t q = 0; q < n_iter; ++q) {
+        if (colorful_out) colorful_out[q] = u64mode ? (double)resu[q] : resf[q];
+        if (colorful_u64_out) colorful_u64_out[q] = u64mode ? resu[q] : (uint64_t)resf[q];
+        if (!u64mode) {
+            if (!std::isfinite(resf[q])) finite = false;
+            sum += resf[q];
+        }
+    }
+    if (estimate) *estimate = u64mode ? std::nan("") : sum / (double)n_iter / (t->P * t->alpha);
+    if (!finite) {
+        set_error("EOVERFLOW: a colourful count is not finite in F32 (use F64 or U64)");
+        return SG2V_EOVERFLOW;
+    }
+    return SG2V_OK;
+}
+
 // Alg. 1 / Alg. 5 outer loop for m templates sharing every colouring (a1 and the
 // colour buckets / histogram once per colouring).
 // colorful[m * n_iter] / colorful_u64[m * n_iter] template-major.
@@ -400,8 +629,12 @@ static sg2v_status count_core(const sg2v_graph *g, const sg2v_template *const *t
     sg2v_options o;
     if (op) o = *op; else if (g_opts_init) o = g_opts; else sg2v_options_default(&o);
     if (o.precision < SG2V_F32 || o.precision > SG2V_U64) { set_error("bad precision"); return SG2V_EINVAL; }
-    if (o.mode != 0 || o.nccl_comm) { set_error("only mode 0 (replicas) is implemented"); return SG2V_EINVAL; }
+    if (o.mode < 0 || o.mode > 1) { set_error("mode must be 0 (replicas) or 1 (vertex partition)"); return SG2V_EINVAL; }
     if (o.iter_stride == 0) o.iter_stride = 1;
+    if (o.mode == 1) {
+        if (m != 1) { set_error("the vertex-partitioned mode counts one template per call"); return SG2V_EINVAL; }
+        return count_vp(g, ts[0], k, n_iter, seed, o, estimates, colorful_out, colorful_u64_out);
+    }
     const int dev = g->device;
     int prev_dev = 0;
     cudaGetDevice(&prev_dev);
@@ -561,6 +794,70 @@ sg2v_status sg2v_workspace_bytes_batch(const sg2v_graph *g, const sg2v_template 
 sg2v_status sg2v_count(const sg2v_graph *g, const sg2v_template *t, int32_t k, int64_t n_iter, uint64_t seed,
                        double *estimate_out, double *colorful_out, uint64_t *colorful_u64_out) {
     return sg2v_count_ex(g, t, k, n_iter, seed, nullptr, estimate_out, colorful_out, colorful_u64_out);
+}
+
+sg2v_status sg2v_comm_unique_id(uint8_t id_out[128]) {
+    if (!id_out) { set_error("NULL argument"); return SG2V_EINVAL; }
+    if (!nccl_api().ok) { set_error("libnccl.so.2 not available"); return SG2V_ENCCL; }
+    ncclUniqueId id;
+    ncclResult_t r = nccl_api().getUniqueId(&id);
+    if (r != ncclSuccess) { set_error(std::string("ncclGetUniqueId: ") + nccl_api().getErrorString(r)); return SG2V_ENCCL; }
+    static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId size");
+    std::memcpy(id_out, &id, 128);
+    return SG2V_OK;
+}
+
+sg2v_status sg2v_comm_init_nccl(const uint8_t id[128], int32_t rank, int32_t world, sg2v_comm **out) {
+    if (!id || !out || world < 1 || rank < 0 || rank >= world) { set_error("bad argument"); return SG2V_EINVAL; }
+    if (!nccl_api().ok) { set_error("libnccl.so.2 not available"); return SG2V_ENCCL; }
+    ncclUniqueId uid;
+    std::memcpy(&uid, id, 128);
+    auto *c = new sg2v_comm();
+    c->rank = rank;
+    c->world = world;
+    ncclResult_t r = nccl_api().commInitRank(&c->nccl, world, uid, rank);
+    if (r != ncclSuccess) {
+        delete c;
+        set_error(std::string("ncclCommInitRank: ") + nccl_api().getErrorString(r));
+        return SG2V_ENCCL;
+    }
+    *out = c;
+    return SG2V_OK;
+}
+
+sg2v_status sg2v_comm_init_callback(int32_t rank, int32_t world, sg2v_allgather_fn fn, void *user, sg2v_comm **out) {
+    if (!fn || !out || world < 1 || rank < 0 || rank >= world) { set_error("bad argument"); return SG2V_EINVAL; }
+    auto *c = new sg2v_comm();
+    c->rank = rank;
+    c->world = world;
+    c->cb = fn;
+    c->user = user;
+    *out = c;
+    return SG2V_OK;
+}
+
+void sg2v_comm_free(sg2v_comm *c) {
+    if (!c) return;
+    if (c->nccl) nccl_api().commDestroy(c->nccl);
+    if (c->hsend) cudaFreeHost(c->hsend);
+    if (c->hrecv) cudaFreeHost(c->hrecv);
+    delete c;
+}
+
+sg2v_status sg2v_graph_load_partition(int64_t n_global, int64_t row_begin, int64_t n_local,
+                                      const int64_t *row_offsets, const int32_t *col_indices, int64_t nnz,
+                                      uint32_t flags, sg2v_graph **out) {
+    if (n_global < 0 || row_begin < 0 || n_local < 0 || row_begin + n_local > n_global) {
+        set_error("partition out of range");
+        return SG2V_EINVAL;
+    }
+    if (flags & SG2V_GRAPH_VALIDATE) { set_error("VALIDATE needs the whole graph (use sg2v_graph_load_csr)"); return SG2V_EINVAL; }
+    sg2v_status st = sg2v_graph_load_csr(n_local, row_offsets, col_indices, nnz, flags, out);
+    if (st != SG2V_OK) return st;
+    (*out)->partitioned = true;
+    (*out)->n_global = n_global;
+    (*out)->row_begin = row_begin;
+    return SG2V_OK;
 }
 
 sg2v_status sg2v_profile_enable(int32_t on) {

@@ -388,7 +388,7 @@ static bool build_index(Plan &pl) {
     std::map<int, int64_t> push_maps;               // anchored push map per passive size p
     for (Step &st : pl.steps) {
         // ---- anchored gather: push map [x][ci][u] -> B column (or -1) ----
-        if (anch && st.src == SRC_GATHER && !(st.top && st.comb == COMB_ACTIVE_LEAF)) {
+        if (anch && st.src == SRC_GATHER && (pl.vp || !(st.top && st.comb == COMB_ACTIVE_LEAF))) {
             auto it = push_maps.find(st.p);
             if (it != push_maps.end()) {
                 st.map_off = it->second;
@@ -415,7 +415,9 @@ static bool build_index(Plan &pl) {
         }
         align();
         st.idx_off = (int64_t)pl.index.size();
-        if (st.top && st.comb == COMB_ACTIVE_LEAF) {
+        if (st.top && st.comb == COMB_ACTIVE_LEAF && pl.vp) {
+            pl.index.push_back(0);  // vertex-partitioned: colorful_i = B(i, [k-1]) from bg (push map above)
+        } else if (st.top && st.comb == COMB_ACTIVE_LEAF) {
             if (!anch) {
                 // colorful_i = B(i, [k] \ {c(i)}): column per colour x
                 for (int x = 0; x < k; ++x) pl.index.push_back((int32_t)colex_rank(full ^ (1u << x)));
@@ -491,8 +493,36 @@ static bool build_index(Plan &pl) {
 
 // Fastest modelled plan whose workspace fits `budget` (0 = unlimited); when no
 // plan fits, the smallest one (sg2v_count then reports ENOMEM with its size).
+// Vertex-partitioned extension: per-rank tables hold the local
+// rows; every gather step all-gathers the passive table in column tiles of
+// tile_w elements into a [n_global][tile_w] staging buffer (double buffered), and
+// pushes into B rows in global memory (bg; the output table itself for
+// leaf-active steps).
+static void plan_vp_extend(Plan &pl, int64_t n_local, int64_t n_global, int64_t tile_req) {
+    const int vn = 16 / pl.elem;
+    int64_t max_cp = 0, max_bg = 0;
+    for (Step &st : pl.steps) {
+        if (st.src != SRC_GATHER) continue;
+        max_cp = std::max(max_cp, round_up(st.cp, vn));
+        const bool bg_is_out = !st.top && st.comb == COMB_ACTIVE_LEAF;
+        if (!bg_is_out) max_bg = std::max(max_bg, st.ldb);
+    }
+    int64_t w = tile_req > 0 ? round_up(tile_req, vn)
+                             : std::max<int64_t>(vn, ((512ll << 20) / std::max<int64_t>(n_global * pl.elem, 1)) / vn * vn);
+    w = std::max<int64_t>(vn, std::min(w, std::max<int64_t>(max_cp, vn)));
+    pl.n_global = n_global;
+    pl.tile_w = w;
+    int64_t off = pl.ws_bytes;
+    pl.off_colors_g = off; off = round_up(off + std::max<int64_t>(n_global, 1) + 16, 256);
+    pl.off_stage = off;    off = round_up(off + 2 * n_global * w * pl.elem, 256);
+    pl.off_send = off;     off = round_up(off + 2 * std::max<int64_t>(n_local, 1) * w * pl.elem, 256);
+    pl.off_bg = off;       off = round_up(off + std::max<int64_t>(n_local, 1) * max_bg * pl.elem, 256);
+    pl.off_part = off;     off = round_up(off + 4096 * 8, 256);
+    pl.ws_bytes = off;
+}
+
 sg2v_status make_plan(const Template &t, int64_t n, int64_t nnz, sg2v_precision prec, Layout layout,
-                      uint64_t budget, std::unique_ptr<Plan> &out) {
+                      uint64_t budget, std::unique_ptr<Plan> &out, int64_t vp_n_global, int64_t vp_tile) {
     std::unique_ptr<Plan> best, smallest;
     int r0 = 0, r1 = t.k - 1;
     if (t.root_hint >= 0) r0 = r1 = t.root_hint;
@@ -512,6 +542,10 @@ sg2v_status make_plan(const Template &t, int64_t n, int64_t nnz, sg2v_precision 
         }
     }
     if (!best) best = std::move(smallest);
+    if (vp_n_global > 0) {
+        best->vp = true;
+        plan_vp_extend(*best, n, vp_n_global, vp_tile);
+    }
     if (!build_index(*best)) return SG2V_ENOMEM;
     out = std::move(best);
     return SG2V_OK;

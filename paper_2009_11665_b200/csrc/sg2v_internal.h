@@ -27,6 +27,18 @@ struct Graph {
     int32_t *d_order = nullptr;  // rows sorted by degree, descending
     uint8_t *d_vclass = nullptr; // floor(log2(1 + rank in degree order)) per vertex (L2 hints)
     int64_t max_deg = 0;
+    // vertex-partitioned mode: this handle holds rows
+    // [row_begin, row_begin + n) of a graph with n_global vertices; col ids are global
+    bool partitioned = false;
+    int64_t n_global = 0, row_begin = 0;
+};
+
+// Column tile / combine descriptor of a vertex-partitioned step.
+struct VpArgs {
+    int mode = 0;               // 1 = tile gather into bg, 2 = combine from bg
+    const char *stage = nullptr;  // [n_global][stage_ld] all-gathered column tile
+    int64_t stage_ld = 0, u0 = 0, cnt = 0;
+    char *bg = nullptr;         // [n_local][ldb]
 };
 
 // ---------------------------------------------------------------------------
@@ -81,6 +93,10 @@ struct Plan {
     int64_t kp = 0;               // anchored: hcnt row stride (int32 colour counts)
     int64_t off_colors = 0, off_hist = 0, off_rowval = 0, off_partial = 0, off_results = 0;
     int64_t off_hcnt = 0, off_bcol = 0;   // anchored: colour counts + colour-bucketed CSR
+    // vertex-partitioned mode: rows are local (n = n_local), colours/staging are global
+    bool vp = false;
+    int64_t n_global = 0, tile_w = 0;      // tile width in elements (multiple of 16 B)
+    int64_t off_stage = 0, off_send = 0, off_bg = 0, off_colors_g = 0, off_part = 0;
     int64_t ws_bytes = 0;
     std::vector<int32_t> index;   // concatenated index tables (host copy)
     int32_t *d_index = nullptr;   // device copy (owned by the template's cache)
@@ -112,7 +128,7 @@ struct Template {
 sg2v_status validate_template(int k, const int32_t *edges, Template &t);
 double automorphisms(const Template &t);
 sg2v_status make_plan(const Template &t, int64_t n, int64_t nnz, sg2v_precision prec, Layout layout,
-                      uint64_t budget, std::unique_ptr<Plan> &out);
+                      uint64_t budget, std::unique_ptr<Plan> &out, int64_t vp_n_global = 0, int64_t vp_tile = 0);
 int64_t binom(int n, int r);
 
 // kernels.cu — launchers; all return cudaError_t as int (0 = success)
@@ -123,6 +139,11 @@ int launch_bucket(const Graph &g, const Plan &pl, const uint8_t *colors, int32_t
                   void *stream);
 int launch_astep(const Graph &g, const Plan &pl, const Step &st, const uint8_t *colors, const int32_t *hcnt,
                  const int32_t *bcol, char *tables, void *rowval, void *stream);
+int launch_astep_vp(const Graph &g, const Plan &pl, const Step &st, const uint8_t *colors, const int32_t *hcnt,
+                    const int32_t *bcol, char *tables, void *rowval, void *stream, const VpArgs *vp);
+int launch_pack_tile(int64_t n, const char *src, int64_t ld_bytes, int64_t u0_bytes, int64_t w_bytes, char *dst,
+                     int64_t dst_ld_bytes, void *stream);
+int launch_bg_rowval(const Plan &pl, int64_t n, const char *bg, int64_t ldb, void *rowval, void *stream);
 int launch_step(const Graph &g, const Plan &pl, const Step &st, const uint8_t *colors,
                 const void *H, char *tables, void *rowval, void *stream);
 int launch_reduce(const Plan &pl, int64_t n, const void *rowval, void *partial, void *result,

@@ -54,7 +54,10 @@ SYMBOLS = ["sg2v_graph_load_csr", "sg2v_graph_free", "sg2v_template_build", "sg2
            "sg2v_template_info", "sg2v_options_default", "sg2v_set_options", "sg2v_workspace_bytes",
            "sg2v_count", "sg2v_count_ex", "sg2v_colorize", "sg2v_plan_describe", "sg2v_plan_describe_n", "sg2v_profile_enable",
            "sg2v_profile_read", "sg2v_last_error", "sg2v_version", "sg2v_count_batch",
-           "sg2v_workspace_bytes_batch"]
+           "sg2v_workspace_bytes_batch", "sg2v_comm_unique_id", "sg2v_comm_init_nccl", "sg2v_comm_init_callback",
+           "sg2v_comm_free", "sg2v_graph_load_partition"]
+
+ALLGATHER_FN = ctypes.CFUNCTYPE(ctypes.c_int32, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_uint64, ctypes.c_void_p)
 
 
 def lib():
@@ -81,6 +84,12 @@ def lib():
         L.sg2v_count_ex.argtypes = [vp, vp, i32, i64, u64, P(Options), vp, vp, vp]
         L.sg2v_colorize.argtypes = [u64, i64, i64, i32, vp, vp]
         L.sg2v_count_batch.argtypes = [vp, vp, i32, i32, i64, u64, P(Options), vp, vp, vp]
+        L.sg2v_comm_unique_id.argtypes = [vp]
+        L.sg2v_comm_init_nccl.argtypes = [vp, i32, i32, P(vp)]
+        L.sg2v_comm_init_callback.argtypes = [i32, i32, ALLGATHER_FN, vp, P(vp)]
+        L.sg2v_comm_free.argtypes = [vp]
+        L.sg2v_comm_free.restype = None
+        L.sg2v_graph_load_partition.argtypes = [i64, i64, i64, vp, vp, i64, ctypes.c_uint32, P(vp)]
         L.sg2v_workspace_bytes_batch.argtypes = [vp, vp, i32, ctypes.c_int, P(u64)]
         L.sg2v_plan_describe.argtypes = [vp, vp, ctypes.c_int, vp, u64, P(u64)]
         L.sg2v_plan_describe_n.argtypes = [i64, i64, vp, ctypes.c_int, vp, u64, P(u64)]
@@ -91,7 +100,8 @@ def lib():
         for name in ("sg2v_graph_load_csr", "sg2v_template_build", "sg2v_template_info", "sg2v_set_options",
                      "sg2v_workspace_bytes", "sg2v_count", "sg2v_count_ex", "sg2v_colorize",
                      "sg2v_plan_describe", "sg2v_plan_describe_n", "sg2v_profile_enable", "sg2v_profile_read",
-                     "sg2v_count_batch", "sg2v_workspace_bytes_batch"):
+                     "sg2v_count_batch", "sg2v_workspace_bytes_batch", "sg2v_comm_unique_id",
+                     "sg2v_comm_init_nccl", "sg2v_comm_init_callback", "sg2v_graph_load_partition"):
             getattr(L, name).restype = ctypes.c_int
         _lib = L
     return _lib
@@ -265,13 +275,14 @@ class Workspace:
 
 def count(graph: Graph, tmpl: Template, n_iter: int, seed: int, precision="f32", iter_offset=0,
           iter_stride=1, workspace: Workspace | None = None, stream=None, row_values=None,
-          allow_overflow=False, mem_budget_bytes=0, layout="anchored"):
+          allow_overflow=False, mem_budget_bytes=0, layout="anchored", comm=None, col_tile=0):
     """sg2v_count_ex.  Returns (estimate, colorful) — colorful is float64[n_iter]
     (F32/F64) or uint64[n_iter] (U64, residues mod 2^64).  row_values: optional
     CUDA tensor (float64 or int64/uint64, n entries) receiving the per-vertex
-    values of the last colouring.  layout: "anchored" (default) or "dense"."""
+    values of the last colouring.  layout: "anchored" (default) or "dense".
+    comm: a Comm -> vertex-partitioned mode (graph from graph_load_partition)."""
     prec = PRECISIONS[precision]
-    if workspace is None and graph.n > 0 and tmpl.k > 1:
+    if workspace is None and graph.n > 0 and tmpl.k > 1 and comm is None:
         workspace = Workspace(workspace_bytes(graph, tmpl, precision, layout, mem_budget_bytes))
     o = Options()
     lib().sg2v_options_default(ctypes.byref(o))
@@ -281,6 +292,10 @@ def count(graph: Graph, tmpl: Template, n_iter: int, seed: int, precision="f32",
     o.stream = stream if stream is not None else _cur_stream()
     o.mem_budget_bytes = int(mem_budget_bytes)
     o.layout = LAYOUTS[layout]
+    if comm is not None:
+        o.mode = 1
+        o.nccl_comm = comm.handle
+        o.col_tile = int(col_tile)
     if workspace is not None:
         o.workspace = workspace.ptr
         o.workspace_bytes = workspace.nbytes
@@ -349,6 +364,79 @@ def count_batch(graph: Graph, tmpls, n_iter: int, seed: int, precision="f32", it
         return est, out
     _check(rc)
     return est, out
+
+
+class Comm:
+    """sg2v_comm: NCCL (Comm.nccl) or host-callback (Comm.callback) transport."""
+
+    def __init__(self, handle, rank, world, keep=None):
+        self._h = handle
+        self.rank = rank
+        self.world = world
+        self._keep = keep
+
+    @property
+    def handle(self):
+        return self._h
+
+    @staticmethod
+    def unique_id() -> bytes:
+        buf = ctypes.create_string_buffer(128)
+        _check(lib().sg2v_comm_unique_id(buf))
+        return buf.raw
+
+    @classmethod
+    def nccl(cls, uid: bytes, rank: int, world: int):
+        buf = ctypes.create_string_buffer(bytes(uid), 128)
+        h = ctypes.c_void_p()
+        _check(lib().sg2v_comm_init_nccl(buf, int(rank), int(world), ctypes.byref(h)))
+        return cls(h, rank, world)
+
+    @classmethod
+    def callback(cls, rank: int, world: int, allgather):
+        """allgather(send: bytes) -> bytes of world*len(send) (rank-major)."""
+        def _fn(send, recv, nbytes, user):
+            try:
+                data = ctypes.string_at(send, nbytes)
+                out = allgather(data)
+                ctypes.memmove(recv, out, len(out))
+                return 0
+            except Exception:
+                return 1
+        cfn = ALLGATHER_FN(_fn)
+        h = ctypes.c_void_p()
+        _check(lib().sg2v_comm_init_callback(int(rank), int(world), cfn, None, ctypes.byref(h)))
+        return cls(h, rank, world, keep=cfn)
+
+    def free(self):
+        if self._h:
+            lib().sg2v_comm_free(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:
+            pass
+
+
+def partition_rows(n_global: int, rank: int, world: int):
+    """Rows of `rank` in the vertex-partitioned mode: [r*nl, r*nl + n_local)."""
+    nl = (n_global + world - 1) // world
+    begin = min(rank * nl, n_global)
+    return begin, max(0, min(nl, n_global - begin))
+
+
+def graph_load_partition(n_global, row_begin, n_local, row_offsets, col_indices, stream=None) -> Graph:
+    """Local rows [row_begin, row_begin+n_local) (host numpy): row_offsets start at 0, global column ids."""
+    ro = np.ascontiguousarray(row_offsets, dtype=np.int64)
+    ci = np.ascontiguousarray(col_indices, dtype=np.int32)
+    o = _set_stream_option(stream)
+    _check(lib().sg2v_set_options(ctypes.byref(o)))
+    h = ctypes.c_void_p()
+    _check(lib().sg2v_graph_load_partition(int(n_global), int(row_begin), int(n_local), ro.ctypes.data,
+                                           ci.ctypes.data if ci.size else None, int(ci.size), 0, ctypes.byref(h)))
+    return Graph(h, int(n_local), int(ci.size))
 
 
 def colorize(seed, j, n, k, out, stream=None):
