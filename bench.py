@@ -48,6 +48,10 @@ def _args():
     p.add_argument("--seed", type=int, default=1)
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--e2e-steps", type=int, default=None)
+    p.add_argument("--mode", default="replicas", choices=["replicas", "vertex"],
+                   help="replicas: colourings sharded over ranks (weak); vertex: every colouring's tables "
+                        "row-partitioned over ranks with NCCL column-tile all-gathers (strong, SURVEY 8(e) V)")
+    p.add_argument("--col-tile", type=int, default=0)
     return p.parse_args()
 
 
@@ -332,10 +336,112 @@ def run_sg2v(args):
     return 0
 
 
+def run_vertex(args):
+    """--mode vertex: 1D vertex partition of every table across the ranks (capacity mode)."""
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    args.gpus = world
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    import paper_2009_11665_b200 as sg
+    from paper_2009_11665_b200.build import build
+    from sg2v_inputs import degree_stats, rmat_1m_like
+
+    build()
+    k, edges = _template(args.template)
+    g = rmat_1m_like(scale=args.scale, seed=args.seed)
+    stats = degree_stats(g)
+    b, nl = sg.partition_rows(g.n, rank, world)
+    ro = np.ascontiguousarray(g.row_offsets[b:b + nl + 1] - g.row_offsets[b])
+    ci = np.ascontiguousarray(g.col_indices[g.row_offsets[b]:g.row_offsets[b + nl]])
+    uid = [sg.Comm.unique_id() if rank == 0 else None]
+    if world > 1:
+        dist.broadcast_object_list(uid, src=0)
+    comm = sg.Comm.nccl(uid[0], rank, world)
+    Gp = sg.graph_load_partition(g.n, b, nl, ro, ci)
+    T = sg.template_build(k, edges)
+    kw = dict(seed=args.seed, precision=args.precision, comm=comm, col_tile=args.col_tile, allow_overflow=True)
+    for t in range(args.warmup):
+        sg.count(Gp, T, n_iter=1, iter_offset=t, **kw)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    stream = torch.cuda.current_stream()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    sg.profile_enable(True)
+    with Clocks(local) as clk:
+        ev0.record(stream)
+        est, c = sg.count(Gp, T, n_iter=args.steps, iter_offset=args.warmup, **kw)
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    prof = sg.profile_read()
+    sg.profile_enable(False)
+    t_max = torch.tensor([ev0.elapsed_time(ev1) / 1e3], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t_max, op=dist.ReduceOp.MAX)
+    value = float(t_max.item()) / args.steps
+    # e2e: partition upload from host + count + read-back, per step
+    e2e_steps = args.e2e_steps if args.e2e_steps is not None else min(args.steps, 2)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for t in range(e2e_steps):
+        Ge = sg.graph_load_partition(g.n, b, nl, ro, ci)
+        sg.count(Ge, T, n_iter=1, iter_offset=args.warmup + args.steps + t, **kw)
+        Ge.free()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    e_max = torch.tensor([e0.elapsed_time(e1) / 1e3], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(e_max, op=dist.ReduceOp.MAX)
+    e2e_value = float(e_max.item()) / max(e2e_steps, 1)
+    comm.free()
+    if rank == 0:
+        peaks = {}
+        try:
+            peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+        except Exception:
+            pass
+        peak = float(peaks.get("hbm_gbs", 6650.0))
+        dom = "step"
+        achieved = prof[dom]["bytes"] / (prof[dom]["ms"] / 1e3) / 1e9 if prof[dom]["ms"] > 0 else 0.0
+        launches = sum(v["launches"] for v in prof.values()) + prof["reduce"]["launches"]
+        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": value * 1e3, "higher_is_better": False, "scaling": "strong",
+                "vs_baseline": None, "dtype": args.precision, "data": "synthetic",
+                "config": {"workload": _workload_name(args, g), "template": args.template, "k": k,
+                           "precision": args.precision, "layout": "anchored", "graph": stats,
+                           "parallelism": f"vertex{world}", "rows_per_rank": nl, "col_tile": args.col_tile,
+                           "l2": "inputs larger than L2; no flush"},
+                "estimate": est, "colorful_first": float(c[0]),
+                "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(ro.nbytes + ci.nbytes),
+                        "d2h_bytes_per_step": 8},
+                "gpu_launches": int(launches),
+                "kernel_ms_per_step": {kk: v["ms"] / args.steps for kk, v in prof.items()},
+                "roofline": {"bound": "hbm", "kernel": "step (tile gathers of rank 0)", "achieved": achieved,
+                             "peak": peak, "unit": "GB/s", "frac": achieved / peak, "traffic": None},
+                "clocks": clk.summary()}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
 def main():
     args = _args()
     if args.impl == "reference":
         return run_reference(args)
+    if args.mode == "vertex":
+        return run_vertex(args)
     return run_sg2v(args)
 
 

@@ -44,7 +44,7 @@ typedef enum {
     SG2V_ENOTTREE = 2,  /* template is not a tree on vertices 0..k-1             */
     SG2V_ENOMEM = 3,    /* workspace would exceed the memory budget (no alloc)   */
     SG2V_ECUDA = 4,     /* CUDA runtime / launch failure, or no sm_100 device    */
-    SG2V_ENCCL = 5,     /* reserved for the vertex-partitioned mode             */
+    SG2V_ENCCL = 5,     /* NCCL / all-gather transport failure (mode 1)          */
     SG2V_EOVERFLOW = 6  /* F32 result not finite (values are still written)      */
 } sg2v_status;
 
@@ -181,7 +181,7 @@ sg2v_status sg2v_workspace_bytes_batch(const sg2v_graph *g, const sg2v_template 
  * Vertex-partitioned mode (SURVEY §8(e) "V": capacity for tables larger than one
  * GPU).  Rank r of W owns rows [r*nl, r*nl + n_local) of G and of every count
  * table, nl = ceil(n_global / W).  Each SpMM step all-gathers the passive table
- * in column tiles (options.col_tile elements; 0 = ~512 MB staging) and every rank
+ * in column tiles (options.col_tile elements; 0 = ~2 GB staging) and every rank
  * pushes its own rows' colour-bucket sums; the eMA and the top step are row-local;
  * the per-rank Σ_i are all-gathered and summed in rank order.  Select it with
  * options.mode = 1 and options.nccl_comm = an sg2v_comm (anchored layout, one

@@ -586,7 +586,9 @@ int launch_astep_vp(const Graph &g, const Plan &pl, const Step &st, const uint8_
     if (pl.prec == SG2V_F32) rc = launch_astep_cfg<float, double>(A, stream);
     else if (pl.prec == SG2V_F64) rc = launch_astep_cfg<double, double>(A, stream);
     else rc = launch_astep_cfg<u64, u64>(A, stream);
-    prof_end(cls, vp ? 0.0 : st.alg_bytes, stream);
+    // algorithmic bytes of a column tile: its share of the step's gather
+    prof_end(cls, !vp ? st.alg_bytes : (vp->mode == 1 ? st.alg_bytes * (double)vp->cnt / (double)std::max<int64_t>(st.cp, 1) : 0.0),
+             stream);
     return rc;
 }
 

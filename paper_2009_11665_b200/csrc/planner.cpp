@@ -508,7 +508,7 @@ static void plan_vp_extend(Plan &pl, int64_t n_local, int64_t n_global, int64_t 
         if (!bg_is_out) max_bg = std::max(max_bg, st.ldb);
     }
     int64_t w = tile_req > 0 ? round_up(tile_req, vn)
-                             : std::max<int64_t>(vn, ((512ll << 20) / std::max<int64_t>(n_global * pl.elem, 1)) / vn * vn);
+                             : std::max<int64_t>(vn, ((2048ll << 20) / std::max<int64_t>(n_global * pl.elem, 1)) / vn * vn);
     w = std::max<int64_t>(vn, std::min(w, std::max<int64_t>(max_cp, vn)));
     pl.n_global = n_global;
     pl.tile_w = w;
