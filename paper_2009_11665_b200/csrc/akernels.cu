@@ -205,7 +205,10 @@ __device__ __forceinline__ void gather_row(const AStepArgs &A, int64_t i, int ci
 // GT threads per row group; R 16-B vectors per thread per pass; U neighbours in
 // flight; V rows per group per slot (V > 1 only for GENERAL non-top steps: each
 // split-table entry is loaded once and applied to V rows).
-template <typename T, typename RT, int GT, int R, int U, int V>
+// MODE: 0 = fused single-GPU step, 1 = vertex-partitioned column-tile gather into
+// bg rows, 2 = vertex-partitioned combine from bg (compile-time so the fused
+// kernel keeps its register allocation).
+template <typename T, typename RT, int GT, int R, int U, int V, int MODE>
 __global__ void __launch_bounds__(256) astep_kernel(AStepArgs A) {
     constexpr int G = 256 / GT;
     constexpr int VN = Vec<T>::N;
@@ -232,7 +235,7 @@ __global__ void __launch_bounds__(256) astep_kernel(AStepArgs A) {
             T *sB = sBase + (size_t)v * A.smem_group;
             T *sA = sB + A.ldb;
             const int64_t i = iv[v];
-            if (A.tile_mode) {
+            if constexpr (MODE == 1) {
                 // vertex-partitioned: push this column tile's R_x sums into the row's
                 // B in global memory (zeroed before the first tile)
                 T *gB = reinterpret_cast<T *>(A.bg) + (size_t)i * A.ldb;
@@ -240,7 +243,7 @@ __global__ void __launch_bounds__(256) astep_kernel(AStepArgs A) {
                 continue;
             }
             if (actv[v]) {
-                if (A.bsrc_global) {
+                if (MODE == 2) {
                     const char *b = A.bg + (size_t)i * A.ldb * sizeof(T);
                     for (int64_t q = t; q < A.ldb / VN; q += GT) reinterpret_cast<uint4 *>(sB)[q] = ldg16(b + q * 16);
                 } else {
@@ -252,9 +255,9 @@ __global__ void __launch_bounds__(256) astep_kernel(AStepArgs A) {
                 }
             }
             group_sync<GT>(g);
-            if (actv[v] && !A.bsrc_global) gather_row<T, GT, R, U>(A, i, (int)A.colors[i], sB, t, g, pol_last, pol_first);
+            if (MODE == 0 && actv[v]) gather_row<T, GT, R, U>(A, i, (int)A.colors[i], sB, t, g, pol_last, pol_first);
         }
-        if (A.tile_mode) {
+        if constexpr (MODE == 1) {
             group_sync<GT>(g);
             continue;
         }
@@ -402,9 +405,9 @@ int launch_bucket(const Graph &g, const Plan &pl, const uint8_t *colors, int32_t
     return (int)cudaGetLastError();
 }
 
-template <typename T, typename RT, int GT, int R, int U, int V = 1>
+template <typename T, typename RT, int GT, int R, int U, int V = 1, int MODE = 0>
 static int launch_astep_t(const AStepArgs &A, void *stream) {
-    auto kern = astep_kernel<T, RT, GT, R, U, V>;
+    auto kern = astep_kernel<T, RT, GT, R, U, V, MODE>;
     constexpr int G = 256 / GT;
     size_t smem = (size_t)G * V * A.smem_group * sizeof(T);
     if (smem > 227 * 1024) return -1;
@@ -428,20 +431,20 @@ static int launch_astep_t(const AStepArgs &A, void *stream) {
 // lane (R = 1) and keep U = 8 neighbours in flight; rows wider than 256 vectors use
 // the whole CTA, one vector per lane per pass with U = 16 neighbours in flight
 // (measured best of R/U in {1/16, 2/8, 4/4} on u15-1, RMAT-1M-like).
-template <typename T, typename RT, int R, int U>
+template <typename T, typename RT, int R, int U, int MODE = 0>
 static int launch_astep_gt(const AStepArgs &A, int gt, void *stream) {
     switch (gt) {
-        case 4: return launch_astep_t<T, RT, 4, R, U>(A, stream);
-        case 8: return launch_astep_t<T, RT, 8, R, U>(A, stream);
-        case 16: return launch_astep_t<T, RT, 16, R, U>(A, stream);
-        case 32: return launch_astep_t<T, RT, 32, R, U>(A, stream);
-        case 64: return launch_astep_t<T, RT, 64, R, U>(A, stream);
-        case 128: return launch_astep_t<T, RT, 128, R, U>(A, stream);
-        default: return launch_astep_t<T, RT, 256, R, U>(A, stream);
+        case 4: return launch_astep_t<T, RT, 4, R, U, 1, MODE>(A, stream);
+        case 8: return launch_astep_t<T, RT, 8, R, U, 1, MODE>(A, stream);
+        case 16: return launch_astep_t<T, RT, 16, R, U, 1, MODE>(A, stream);
+        case 32: return launch_astep_t<T, RT, 32, R, U, 1, MODE>(A, stream);
+        case 64: return launch_astep_t<T, RT, 64, R, U, 1, MODE>(A, stream);
+        case 128: return launch_astep_t<T, RT, 128, R, U, 1, MODE>(A, stream);
+        default: return launch_astep_t<T, RT, 256, R, U, 1, MODE>(A, stream);
     }
 }
 
-template <typename T, typename RT>
+template <typename T, typename RT, int MODE = 0>
 static int launch_astep_cfg(const AStepArgs &A0, void *stream) {
     AStepArgs A = A0;
     constexpr int VN = Vec<T>::N;
@@ -463,6 +466,14 @@ static int launch_astep_cfg(const AStepArgs &A0, void *stream) {
     // eMA-heavy GENERAL steps: V = 4 rows share every split-table load
     const bool multi = A.comb == COMB_GENERAL && !A.top && A.nterms >= 8 && gt >= 32 && tune != 5 &&
                        (size_t)(256 / gt) * 4 * A.smem_group * sizeof(T) <= 200 * 1024;
+    if constexpr (MODE != 0) {
+        if (multi && MODE == 2) {
+            if (nvec > 256) return launch_astep_t<T, RT, 256, 1, 16, 4, MODE>(A, stream);
+            return launch_astep_t<T, RT, 256, 1, 8, 4, MODE>(A, stream);
+        }
+        if (nvec > 256) return launch_astep_t<T, RT, 256, 1, 16, 1, MODE>(A, stream);
+        return launch_astep_gt<T, RT, 1, 8, MODE>(A, gt, stream);
+    }
     if (multi) {
         if (nvec > 256) return launch_astep_t<T, RT, 256, 1, 16, 4>(A, stream);
         switch (gt) {
@@ -543,7 +554,9 @@ int launch_astep_vp(const Graph &g, const Plan &pl, const Step &st, const uint8_
     A.bsrc_global = 0;
     A.bg = nullptr;
     // stage M_a next to B only while both fit comfortably (occupancy); else L1
-    A.stage_a = (st.comb == COMB_GENERAL) && (st.ldb + st.lda) * pl.elem <= 100 * 1024;
+    static int stage_kb = -1;  // SG2V_STAGE_KB (experiments): M_a staging threshold
+    if (stage_kb < 0) { const char *e = getenv("SG2V_STAGE_KB"); stage_kb = e ? atoi(e) : 100; }
+    A.stage_a = (st.comb == COMB_GENERAL) && (st.ldb + st.lda) * pl.elem <= (int64_t)stage_kb * 1024;
     A.tpo = 1;  // set per launch configuration (launch_astep_cfg)
     A.smem_group = st.ldb + (A.stage_a ? st.lda : 0);
     A.tagged = g.n < (int64_t(1) << kClassShift);
@@ -583,9 +596,16 @@ int launch_astep_vp(const Graph &g, const Plan &pl, const Step &st, const uint8_
     int cls = st.top ? 3 : 2;
     prof_begin(cls, stream);
     int rc;
-    if (pl.prec == SG2V_F32) rc = launch_astep_cfg<float, double>(A, stream);
-    else if (pl.prec == SG2V_F64) rc = launch_astep_cfg<double, double>(A, stream);
-    else rc = launch_astep_cfg<u64, u64>(A, stream);
+    const int md = vp ? vp->mode : 0;
+    if (pl.prec == SG2V_F32)
+        rc = md == 1 ? launch_astep_cfg<float, double, 1>(A, stream)
+                     : md == 2 ? launch_astep_cfg<float, double, 2>(A, stream) : launch_astep_cfg<float, double, 0>(A, stream);
+    else if (pl.prec == SG2V_F64)
+        rc = md == 1 ? launch_astep_cfg<double, double, 1>(A, stream)
+                     : md == 2 ? launch_astep_cfg<double, double, 2>(A, stream) : launch_astep_cfg<double, double, 0>(A, stream);
+    else
+        rc = md == 1 ? launch_astep_cfg<u64, u64, 1>(A, stream)
+                     : md == 2 ? launch_astep_cfg<u64, u64, 2>(A, stream) : launch_astep_cfg<u64, u64, 0>(A, stream);
     // algorithmic bytes of a column tile: its share of the step's gather
     prof_end(cls, !vp ? st.alg_bytes : (vp->mode == 1 ? st.alg_bytes * (double)vp->cnt / (double)std::max<int64_t>(st.cp, 1) : 0.0),
              stream);
