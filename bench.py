@@ -189,6 +189,30 @@ def run_reference(args):
 
 
 # --------------------------------------------------------------------------- GPU arm
+def _setup_dist(world, local):
+    """One rank per GPU over NCCL.  SG2V_BENCH_SHARED_GPU=1 (tests only) lets several
+    ranks share the visible GPUs, with gloo for the (CPU) collectives."""
+    import torch
+    import torch.distributed as dist
+    shared = os.environ.get("SG2V_BENCH_SHARED_GPU") == "1"
+    dev = local % max(torch.cuda.device_count(), 1) if shared else local
+    torch.cuda.set_device(dev)
+    if world > 1:
+        if shared:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
+    return dev
+
+
+def _dist_device():
+    import torch
+    import torch.distributed as dist
+    if dist.is_initialized() and dist.get_backend() == "gloo":
+        return "cpu"
+    return "cuda"
+
+
 def run_sg2v(args):
     import numpy as np
     import torch
@@ -199,9 +223,7 @@ def run_sg2v(args):
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world != args.gpus:
         args.gpus = world
-    torch.cuda.set_device(local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = _setup_dist(world, local)
 
     import paper_2009_11665_b200 as sg
     from paper_2009_11665_b200.build import build
@@ -233,10 +255,10 @@ def run_sg2v(args):
         dist.barrier()
 
     # ---- timed region: K colourings per rank, device time (CUDA events) ----
-    counts = torch.zeros(world * args.steps, dtype=torch.float64, device="cuda")
+    counts = torch.zeros(world * args.steps, dtype=torch.float64, device=_dist_device())
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     sg.profile_enable(True)
-    with Clocks(local) as clk:
+    with Clocks(dev) as clk:
         torch.cuda.synchronize()
         ev0.record(stream)
         est, c = sg.count(G, T, n_iter=args.steps, seed=args.seed, iter_offset=colouring(args.warmup),
@@ -250,7 +272,7 @@ def run_sg2v(args):
     prof = sg.profile_read()
     sg.profile_enable(False)
     dev_s = ev0.elapsed_time(ev1) / 1e3
-    t_max = torch.tensor([dev_s], dtype=torch.float64, device="cuda")
+    t_max = torch.tensor([dev_s], dtype=torch.float64, device=_dist_device())
     if world > 1:
         dist.all_reduce(t_max, op=dist.ReduceOp.MAX)
     total = world * args.steps
@@ -271,7 +293,7 @@ def run_sg2v(args):
         Ge.free()
     e1.record(stream)
     torch.cuda.synchronize()
-    e_max = torch.tensor([e0.elapsed_time(e1) / 1e3], dtype=torch.float64, device="cuda")
+    e_max = torch.tensor([e0.elapsed_time(e1) / 1e3], dtype=torch.float64, device=_dist_device())
     if world > 1:
         dist.all_reduce(e_max, op=dist.ReduceOp.MAX)
     e2e_value = float(e_max.item()) / (world * max(e2e_steps, 1))
@@ -346,9 +368,7 @@ def run_vertex(args):
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     args.gpus = world
-    torch.cuda.set_device(local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = _setup_dist(world, local)
     import paper_2009_11665_b200 as sg
     from paper_2009_11665_b200.build import build
     from sg2v_inputs import degree_stats, rmat_1m_like
@@ -375,14 +395,14 @@ def run_vertex(args):
     stream = torch.cuda.current_stream()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     sg.profile_enable(True)
-    with Clocks(local) as clk:
+    with Clocks(dev) as clk:
         ev0.record(stream)
         est, c = sg.count(Gp, T, n_iter=args.steps, iter_offset=args.warmup, **kw)
         ev1.record(stream)
         torch.cuda.synchronize()
     prof = sg.profile_read()
     sg.profile_enable(False)
-    t_max = torch.tensor([ev0.elapsed_time(ev1) / 1e3], dtype=torch.float64, device="cuda")
+    t_max = torch.tensor([ev0.elapsed_time(ev1) / 1e3], dtype=torch.float64, device=_dist_device())
     if world > 1:
         dist.all_reduce(t_max, op=dist.ReduceOp.MAX)
     value = float(t_max.item()) / args.steps
@@ -399,7 +419,7 @@ def run_vertex(args):
         Ge.free()
     e1.record(stream)
     torch.cuda.synchronize()
-    e_max = torch.tensor([e0.elapsed_time(e1) / 1e3], dtype=torch.float64, device="cuda")
+    e_max = torch.tensor([e0.elapsed_time(e1) / 1e3], dtype=torch.float64, device=_dist_device())
     if world > 1:
         dist.all_reduce(e_max, op=dist.ReduceOp.MAX)
     e2e_value = float(e_max.item()) / max(e2e_steps, 1)
