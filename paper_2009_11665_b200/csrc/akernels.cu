@@ -171,13 +171,28 @@ __device__ __forceinline__ void gather_row(const AStepArgs &A, int64_t i, int ci
 #pragma unroll
                         for (int q = 0; q < R; ++q) Vec<T>::add(acc[q], xv[u][q]);
                 }
-                for (; e2 < e3; ++e2) {
-                    const int32_t b1 = __ldg(A.bcol + e2);
-                    const int32_t j1 = A.tagged ? (b1 & kIdMask) : b1;
+                if (e2 < e3) {  // tail: one predicated batch, all loads in flight together
+                    constexpr int UT = U < 8 ? U : 8;
+                    for (; e2 < e3; e2 += UT) {
+                        int32_t jj[UT];
 #pragma unroll
-                    for (int q = 0; q < R; ++q) {
-                        const int64_t v = v0 + q * GT + t;
-                        if (v < nvec_p) Vec<T>::add(acc[q], ldg16(A.mp + (size_t)j1 * row_bytes + v * 16));
+                        for (int u = 0; u < UT; ++u) {
+                            const int32_t b1 = (e2 + u < e3) ? __ldg(A.bcol + e2 + u) : -1;
+                            jj[u] = (b1 >= 0 && A.tagged) ? (b1 & kIdMask) : b1;
+                        }
+                        uint4 xv[UT][R];
+#pragma unroll
+                        for (int u = 0; u < UT; ++u)
+#pragma unroll
+                            for (int q = 0; q < R; ++q) {
+                                const int64_t v = v0 + q * GT + t;
+                                xv[u][q] = (jj[u] >= 0 && v < nvec_p) ? ldg16(A.mp + (size_t)jj[u] * row_bytes + v * 16)
+                                                                      : make_uint4(0, 0, 0, 0);
+                            }
+#pragma unroll
+                        for (int u = 0; u < UT; ++u)
+#pragma unroll
+                            for (int q = 0; q < R; ++q) Vec<T>::add(acc[q], xv[u][q]);
                     }
                 }
                 // push R_x into B: distinct targets within one colour
