@@ -15,6 +15,8 @@
 #include <cstring>
 #include <functional>
 #include <limits>
+#include <map>
+#include <set>
 #include <sstream>
 
 #include "sg2v_internal.h"
@@ -254,9 +256,57 @@ static bool plan_chain(const Template &t, const Chain &c, int root, int64_t n, i
         seq.push_back(v);
         return std::min(first_a, first_p);
     };
-    order(c.top, sched);
+    {
+        std::vector<int> full;
+        order(c.top, full);
+        (void)full;
+    }
+    // --- isomorphic rooted sub-templates share one table ---------------------
+    // M_s(i, S) counts colourful embeddings of the ROOTED sub-template T_s with
+    // its root at i, so it depends only on T_s's rooted isomorphism
+    // class: compute each class once (e.g. the two arms of a path rooted at its
+    // middle) and let every parent read it.  canon(node) = AHU string of the
+    // rooted sub-template (children multiset, sorted).
+    std::vector<std::string> canon(pl.nodes.size());
+    {
+        std::vector<std::vector<std::string>> kids(pl.nodes.size());
+        for (size_t v = 0; v < pl.nodes.size(); ++v) {  // children precede parents
+            const Node &nd = pl.nodes[v];
+            if (nd.active >= 0) {
+                kids[v] = kids[nd.active];
+                kids[v].push_back(canon[nd.passive]);
+                std::sort(kids[v].begin(), kids[v].end());
+            }
+            std::string cs = "(";
+            for (auto &x : kids[v]) cs += x;
+            canon[v] = cs + ")";
+        }
+    }
+    {
+        std::set<std::string> done;
+        std::function<void(int)> visit = [&](int v) {
+            const Node &nd = pl.nodes[v];
+            if (nd.active < 0 || done.count(canon[v])) return;
+            // Sethi–Ullman child order of the tree without sharing
+            std::vector<int> sa, sp;
+            int64_t pa = order(nd.active, sa), pp = order(nd.passive, sp);
+            int64_t oa = out_bytes[nd.active], op = out_bytes[nd.passive];
+            if (std::max(pa, oa + pp) <= std::max(pp, op + pa)) { visit(nd.active); visit(nd.passive); }
+            else { visit(nd.passive); visit(nd.active); }
+            done.insert(canon[v]);
+            sched.push_back(v);
+        };
+        visit(c.top);
+    }
+    // uses of each class by the scheduled steps (a table is freed after its last use)
+    std::map<std::string, int> uses;
+    for (int v : sched) {
+        uses[canon[pl.nodes[v].active]]++;
+        uses[canon[pl.nodes[v].passive]]++;
+    }
 
     // --- first-fit arena over the schedule ---
+    std::map<std::string, int> class_buf;   // canon -> buffer
     std::vector<int> node_buf(pl.nodes.size(), -1);
     std::vector<std::pair<int64_t, int64_t>> live;  // (offset, bytes)
     int64_t arena = 0;
@@ -296,8 +346,8 @@ static bool plan_chain(const Template &t, const Chain &c, int root, int64_t n, i
         st.lda = round_up(st.ca, vn);
         st.ldp = (st.src == SRC_HIST) ? round_up(k, vn) : round_up(st.cp, vn);
         st.ldb = anch ? round_up(st.cb, vn) : st.ldp;
-        st.buf_a = node_buf[nd.active];
-        st.buf_p = node_buf[nd.passive];
+        st.buf_a = class_buf.count(canon[nd.active]) ? class_buf[canon[nd.active]] : -1;
+        st.buf_p = class_buf.count(canon[nd.passive]) ? class_buf[canon[nd.passive]] : -1;
         if (st.src == SRC_HIST && !anch) pl.need_hist = true;
         if (!st.top) {
             Buffer b;
@@ -306,9 +356,10 @@ static bool plan_chain(const Template &t, const Chain &c, int root, int64_t n, i
             pl.bufs.push_back(b);
             st.buf_out = (int)pl.bufs.size() - 1;
             node_buf[v] = st.buf_out;
+            class_buf[canon[v]] = st.buf_out;
         }
-        release(st.buf_a);
-        release(st.buf_p);
+        if (--uses[canon[nd.active]] == 0) release(st.buf_a);
+        if (--uses[canon[nd.passive]] == 0) release(st.buf_p);
 
         // algorithmic bytes (useful columns only) and the model (sector-rounded)
         double bytes = 0.0, mbytes = 0.0;
