@@ -114,6 +114,8 @@ struct AStepArgs {
     int packed;         // split pairs packed as ia | ip << 16 (both < 2^16)
     int stage_a;        // M_a row staged in shared memory (else read through L1)
     int tpo;            // lanes per output in the eMA (power of 2, <= 32)
+    int64_t aoff;       // offset of the M_a row in a group's shared memory: ldb, or 0 when
+                        // M_a(i,·) IS B(i,·) (self step: T_s = root + two copies of X)
     // vertex-partitioned mode: B rows live in global memory
     int64_t cp_map;     // row length of the push map (= cp unless tiled)
     int64_t u0;         // first passive column of this tile (push-map offset)
@@ -264,7 +266,7 @@ __global__ void __launch_bounds__(256) astep_kernel(AStepArgs A) {
                 } else {
                     for (int64_t q = t; q < A.ldb / VN; q += GT) reinterpret_cast<uint4 *>(sB)[q] = make_uint4(0, 0, 0, 0);
                 }
-                if (A.comb == COMB_GENERAL && A.stage_a) {
+                if (A.comb == COMB_GENERAL && A.stage_a && A.aoff != 0) {
                     const char *a = A.ma + (size_t)i * A.lda * sizeof(T);
                     for (int64_t q = t; q < A.lda / VN; q += GT) reinterpret_cast<uint4 *>(sA)[q] = ldg16(a + q * 16);
                 }
@@ -310,7 +312,7 @@ __global__ void __launch_bounds__(256) astep_kernel(AStepArgs A) {
 #pragma unroll
                             for (int v = 0; v < V; ++v) {
                                 const T *sB = sBase + (size_t)v * A.smem_group;
-                                acc[v] += sB[A.ldb + ia] * sB[ib];
+                                acc[v] += sB[A.aoff + ia] * sB[ib];
                             }
                         }
                     } else {
@@ -328,7 +330,7 @@ __global__ void __launch_bounds__(256) astep_kernel(AStepArgs A) {
 #pragma unroll
                             for (int v = 0; v < V; ++v) {
                                 const T *sB = sBase + (size_t)v * A.smem_group;
-                                const T av = A.stage_a ? sB[A.ldb + ia]
+                                const T av = A.stage_a ? sB[A.aoff + ia]
                                                        : __ldg(reinterpret_cast<const T *>(A.ma) + (size_t)iv[v] * A.lda + ia);
                                 acc[v] += av * sB[ib];
                             }
@@ -361,7 +363,7 @@ __global__ void __launch_bounds__(256) astep_kernel(AStepArgs A) {
                     ia = q.x;
                     ib = q.y;
                 }
-                const T av = A.stage_a ? sB[A.ldb + ia] : __ldg(ga + ia);
+                const T av = A.stage_a ? sB[A.aoff + ia] : __ldg(ga + ia);
                 racc += (RT)av * (RT)sB[ib];
             }
         }
@@ -550,7 +552,7 @@ int launch_astep_vp(const Graph &g, const Plan &pl, const Step &st, const uint8_
     A.cp = st.cp;
     A.src_hist = st.src == SRC_HIST;
     A.pmap = st.map_off >= 0 ? pl.d_index + st.map_off : nullptr;
-    A.ma = (st.comb == COMB_GENERAL) ? tables + pl.bufs[st.buf_a].offset : nullptr;
+    A.ma = (st.comb == COMB_GENERAL && st.buf_a >= 0) ? tables + pl.bufs[st.buf_a].offset : nullptr;
     A.lda = st.lda;
     A.ms = st.top ? nullptr : tables + pl.bufs[st.buf_out].offset;
     A.lds = st.lds;
@@ -569,11 +571,12 @@ int launch_astep_vp(const Graph &g, const Plan &pl, const Step &st, const uint8_
     A.bsrc_global = 0;
     A.bg = nullptr;
     // stage M_a next to B only while both fit comfortably (occupancy); else L1
+    A.aoff = st.self_a ? 0 : st.ldb;
     static int stage_kb = -1;  // SG2V_STAGE_KB (experiments): M_a staging threshold
     if (stage_kb < 0) { const char *e = getenv("SG2V_STAGE_KB"); stage_kb = e ? atoi(e) : 100; }
-    A.stage_a = (st.comb == COMB_GENERAL) && (st.ldb + st.lda) * pl.elem <= (int64_t)stage_kb * 1024;
+    A.stage_a = (st.comb == COMB_GENERAL) && (st.self_a || (st.ldb + st.lda) * pl.elem <= (int64_t)stage_kb * 1024);
     A.tpo = 1;  // set per launch configuration (launch_astep_cfg)
-    A.smem_group = st.ldb + (A.stage_a ? st.lda : 0);
+    A.smem_group = st.ldb + (A.stage_a && !st.self_a ? st.lda : 0);
     A.tagged = g.n < (int64_t(1) << kClassShift);
     {
         // rows of the hottest H neighbours fit in ~75 MB of the 126 MB L2

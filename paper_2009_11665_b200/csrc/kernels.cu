@@ -412,7 +412,7 @@ int launch_step(const Graph &g, const Plan &pl, const Step &st, const uint8_t *c
     A.src = src;
     A.ldp = st.ldp;
     A.src_hist = st.src == SRC_HIST;
-    A.ma = (st.comb == COMB_GENERAL) ? tables + pl.bufs[st.buf_a].offset : nullptr;
+    A.ma = (st.comb == COMB_GENERAL && st.buf_a >= 0) ? tables + pl.bufs[st.buf_a].offset : nullptr;
     A.lda = st.lda;
     A.ms = st.top ? nullptr : tables + pl.bufs[st.buf_out].offset;
     A.lds = st.lds;

@@ -282,11 +282,29 @@ static bool plan_chain(const Template &t, const Chain &c, int root, int64_t n, i
             canon[v] = cs + ")";
         }
     }
+    // Self steps (anchored): T_s = root ρ + two isomorphic child subtrees X, split as
+    // active = ρ + X (itself leaf-active over X) and passive = X.  The active row is
+    // M_a(i,·) = B_X(i,·) with the same [k-1]-subset indexing as the step's own
+    // B_X(i,·) (anchored leaf-active identity), so one gather of X's table gives both:
+    // M_s(i,S) = Σ_{A⊂S} B_X(i,A)·B_X(i,S∖A).  The ρ + X table is never built.
+    auto self_step = [&](int v) -> bool {
+        if (!anch) return false;
+        const Node &nd = pl.nodes[v];
+        if (nd.active < 0) return false;
+        const Node &na = pl.nodes[nd.active];
+        return na.active >= 0 && pl.nodes[na.active].active < 0 && canon[na.passive] == canon[nd.passive];
+    };
     {
         std::set<std::string> done;
         std::function<void(int)> visit = [&](int v) {
             const Node &nd = pl.nodes[v];
             if (nd.active < 0 || done.count(canon[v])) return;
+            if (self_step(v)) {  // the active child is never materialised
+                visit(nd.passive);
+                done.insert(canon[v]);
+                sched.push_back(v);
+                return;
+            }
             // Sethi–Ullman child order of the tree without sharing
             std::vector<int> sa, sp;
             int64_t pa = order(nd.active, sa), pp = order(nd.passive, sp);
@@ -301,7 +319,7 @@ static bool plan_chain(const Template &t, const Chain &c, int root, int64_t n, i
     // uses of each class by the scheduled steps (a table is freed after its last use)
     std::map<std::string, int> uses;
     for (int v : sched) {
-        uses[canon[pl.nodes[v].active]]++;
+        if (!self_step(v)) uses[canon[pl.nodes[v].active]]++;
         uses[canon[pl.nodes[v].passive]]++;
     }
 
@@ -346,7 +364,8 @@ static bool plan_chain(const Template &t, const Chain &c, int root, int64_t n, i
         st.lda = round_up(st.ca, vn);
         st.ldp = (st.src == SRC_HIST) ? round_up(k, vn) : round_up(st.cp, vn);
         st.ldb = anch ? round_up(st.cb, vn) : st.ldp;
-        st.buf_a = class_buf.count(canon[nd.active]) ? class_buf[canon[nd.active]] : -1;
+        st.self_a = self_step(v);
+        st.buf_a = (!st.self_a && class_buf.count(canon[nd.active])) ? class_buf[canon[nd.active]] : -1;
         st.buf_p = class_buf.count(canon[nd.passive]) ? class_buf[canon[nd.passive]] : -1;
         if (st.src == SRC_HIST && !anch) pl.need_hist = true;
         if (!st.top) {
@@ -358,7 +377,7 @@ static bool plan_chain(const Template &t, const Chain &c, int root, int64_t n, i
             node_buf[v] = st.buf_out;
             class_buf[canon[v]] = st.buf_out;
         }
-        if (--uses[canon[nd.active]] == 0) release(st.buf_a);
+        if (!st.self_a && --uses[canon[nd.active]] == 0) release(st.buf_a);
         if (--uses[canon[nd.passive]] == 0) release(st.buf_p);
 
         // algorithmic bytes (useful columns only) and the model (sector-rounded)
@@ -379,7 +398,7 @@ static bool plan_chain(const Template &t, const Chain &c, int root, int64_t n, i
             double mg = (st.src == SRC_GATHER)
                             ? nnz * 4.0 + nnz * live_frac * (double)round_up(st.cp * pl.elem, 32) + n * 12.0
                             : hsrc;
-            double ma = (st.comb == COMB_GENERAL) ? n * (double)st.ca * E : n * 1.0;
+            double ma = (st.comb == COMB_GENERAL && !st.self_a) ? n * (double)st.ca * E : n * 1.0;
             double w = st.top ? n * 8.0 : n * (double)st.cs * E;
             bytes = gather + ma + w;
             mbytes = mg + ma + w;
@@ -618,7 +637,7 @@ std::string Plan::describe() const {
           << ",\"comb\":\"" << (s.comb == COMB_ACTIVE_LEAF ? "active_leaf" : "general") << "\""
           << ",\"cs\":" << s.cs << ",\"ca\":" << s.ca << ",\"cp\":" << s.cp
           << ",\"cb\":" << s.cb << ",\"lds\":" << s.lds << ",\"ldp\":" << s.ldp << ",\"nterms\":" << s.nterms
-          << ",\"gt\":" << s.gt << ",\"alg_bytes\":" << s.alg_bytes << ",\"ema_terms\":" << s.ema_terms << "}";
+          << ",\"self\":" << (s.self_a ? "true" : "false") << ",\"gt\":" << s.gt << ",\"alg_bytes\":" << s.alg_bytes << ",\"ema_terms\":" << s.ema_terms << "}";
     }
     o << "]}";
     return o.str();

@@ -142,10 +142,11 @@ def test_isomorphic_subtemplates_share_tables():
     # (M_s depends only on the rooted isomorphism class of T_s)
     T15 = sg.template_build(15, path_template(15), root_hint=7)
     d = sg.plan_describe_n(1 << 20, 200 << 20, T15, "f32")
-    assert len(d["steps"]) == 8 and d["steps"][-1]["s"] == 15
+    # arm 2..7 once, then the top 15 = (7 + 7-arm) + 7-arm as a self step (one gather)
+    assert len(d["steps"]) == 7 and d["steps"][-1]["s"] == 15 and d["steps"][-1]["self"]
     T12 = sg.template_build(12, path_template(12), root_hint=5)
     d = sg.plan_describe_n(1 << 20, 200 << 20, T12, "f32")
     assert [(s["s"], s["a"], s["p"]) for s in d["steps"]][-1] == (12, 6, 6) and len(d["steps"]) == 6
-    # stars: every leaf arm is the same class, but each star step is distinct
+    # stars: every leaf arm is the same class; the first split (centre + 2 leaves) is a self step
     S = sg.template_build(9, star_template(9))
-    assert len(sg.plan_describe_n(1000, 8000, S, "u64")["steps"]) == 8
+    assert len(sg.plan_describe_n(1000, 8000, S, "u64")["steps"]) == 7  # 3 = 1 + 2 leaves is a self step
