@@ -125,7 +125,8 @@ struct AStepArgs {
 };
 
 // ---- stage 1 for one row: B(i,·) over T ⊂ [k]∖{c(i)} into sB (group-uniform) ----
-template <typename T, int GT, int R, int U>
+// STRIDE: element stride of B in sB (V when V rows are interleaved in shared memory)
+template <typename T, int GT, int R, int U, int STRIDE = 1>
 __device__ __forceinline__ void gather_row(const AStepArgs &A, int64_t i, int ci, T *sB, int t, int g,
                                            uint64_t pol_last, uint64_t pol_first) {
     constexpr int VN = Vec<T>::N;
@@ -135,7 +136,7 @@ __device__ __forceinline__ void gather_row(const AStepArgs &A, int64_t i, int ci
     const int k = A.k;
     const int32_t *h = A.hcnt + (size_t)i * A.kp;
     if (A.src_hist) {
-        for (int64_t y = t; y < A.cb; y += GT) sB[y] = (T)__ldg(h + y + (y >= ci ? 1 : 0));
+        for (int64_t y = t; y < A.cb; y += GT) sB[y * STRIDE] = (T)__ldg(h + y + (y >= ci ? 1 : 0));
         return;
     }
     int64_t e = A.rowptr[i];
@@ -207,7 +208,7 @@ __device__ __forceinline__ void gather_row(const AStepArgs &A, int64_t i, int ci
                             const int64_t u = v * VN + el;
                             if (u < A.cp) {
                                 const int32_t tt = __ldg(mp + u);
-                                if (tt >= 0) sB[tt] += vget<T>(acc[q], el);
+                                if (tt >= 0) sB[(size_t)tt * STRIDE] += vget<T>(acc[q], el);
                             }
                         }
                     }
@@ -247,19 +248,22 @@ __global__ void __launch_bounds__(256) astep_kernel(AStepArgs A) {
             iv[v] = actv[v] ? A.order[r] : 0;
         }
         // ---- stage 1: B rows (and staged M_a rows) into shared memory -----------
-#pragma unroll
-        for (int v = 0; v < V; ++v) {
-            T *sB = sBase + (size_t)v * A.smem_group;
+        // V = 1: [B | M_a] per group.  V > 1: the V rows are interleaved element by
+        // element ([ldb][V] then [lda][V]) so one 16-byte shared load fetches an entry
+        // of all V rows in the eMA.
+        if constexpr (V == 1) {
+            T *sB = sBase;
             T *sA = sB + A.ldb;
-            const int64_t i = iv[v];
+            const int64_t i = iv[0];
             if constexpr (MODE == 1) {
                 // vertex-partitioned: push this column tile's R_x sums into the row's
                 // B in global memory (zeroed before the first tile)
                 T *gB = reinterpret_cast<T *>(A.bg) + (size_t)i * A.ldb;
-                if (actv[v]) gather_row<T, GT, R, U>(A, i, (int)A.colors[i], gB, t, g, pol_last, pol_first);
+                if (actv[0]) gather_row<T, GT, R, U>(A, i, (int)A.colors[i], gB, t, g, pol_last, pol_first);
+                group_sync<GT>(g);
                 continue;
             }
-            if (actv[v]) {
+            if (actv[0]) {
                 if (MODE == 2) {
                     const char *b = A.bg + (size_t)i * A.ldb * sizeof(T);
                     for (int64_t q = t; q < A.ldb / VN; q += GT) reinterpret_cast<uint4 *>(sB)[q] = ldg16(b + q * 16);
@@ -272,11 +276,33 @@ __global__ void __launch_bounds__(256) astep_kernel(AStepArgs A) {
                 }
             }
             group_sync<GT>(g);
-            if (MODE == 0 && actv[v]) gather_row<T, GT, R, U>(A, i, (int)A.colors[i], sB, t, g, pol_last, pol_first);
-        }
-        if constexpr (MODE == 1) {
+            if (MODE == 0 && actv[0]) gather_row<T, GT, R, U>(A, i, (int)A.colors[i], sB, t, g, pol_last, pol_first);
+        } else {
+            static_assert(MODE != 1, "tile mode runs one row per group");
+#pragma unroll
+            for (int v = 0; v < V; ++v) {
+                const int64_t i = iv[v];
+                if (actv[v]) {
+                    if (MODE == 2) {
+                        const T *b = reinterpret_cast<const T *>(A.bg) + (size_t)i * A.ldb;
+                        for (int64_t q = t; q < A.ldb; q += GT) sBase[q * V + v] = b[q];
+                    } else {
+                        for (int64_t q = t; q < A.ldb; q += GT) sBase[q * V + v] = 0;
+                    }
+                    if (A.comb == COMB_GENERAL && A.stage_a && A.aoff != 0) {
+                        const T *a = reinterpret_cast<const T *>(A.ma) + (size_t)i * A.lda;
+                        for (int64_t q = t; q < A.lda; q += GT) sBase[(A.ldb + q) * V + v] = __ldg(a + q);
+                    }
+                } else {
+                    for (int64_t q = t; q < A.ldb + A.lda; q += GT) sBase[q * V + v] = 0;
+                }
+            }
             group_sync<GT>(g);
-            continue;
+            if (MODE == 0) {
+#pragma unroll
+                for (int v = 0; v < V; ++v)
+                    if (actv[v]) gather_row<T, GT, R, U, V>(A, iv[v], (int)A.colors[iv[v]], sBase + v, t, g, pol_last, pol_first);
+            }
         }
         group_sync<GT>(g);
         // ---- stage 2: eMA over the universe [k-1] ------------------------------
@@ -303,7 +329,25 @@ __global__ void __launch_bounds__(256) astep_kernel(AStepArgs A) {
 #pragma unroll
                 for (int v = 0; v < V; ++v) acc[v] = 0;
                 if (o < cs) {
-                    if (A.packed && A.stage_a) {
+                    if (V > 1 && A.packed && A.stage_a) {
+                        // interleaved rows: entry e of the V rows is sBase[e*V .. e*V+V)
+                        const uint32_t *p = reinterpret_cast<const uint32_t *>(A.idx) + o;
+                        constexpr int NV = (V * (int)sizeof(T)) / 16;  // 16-B vectors per entry
+#pragma unroll 16
+                        for (int w = l; w < nt; w += tpo) {
+                            const uint32_t q = __ldg(p + w * cs);
+                            const uint32_t ia = (q & 0xffffu) + (uint32_t)A.aoff, ib = q >> 16;
+                            const uint4 *pa = reinterpret_cast<const uint4 *>(sBase + (size_t)ia * V);
+                            const uint4 *pb = reinterpret_cast<const uint4 *>(sBase + (size_t)ib * V);
+#pragma unroll
+                            for (int z = 0; z < NV; ++z) {
+                                const uint4 va = pa[z], vb = pb[z];
+#pragma unroll
+                                for (int e = 0; e < 16 / (int)sizeof(T); ++e)
+                                    acc[z * (16 / (int)sizeof(T)) + e] += vget<T>(va, e) * vget<T>(vb, e);
+                            }
+                        }
+                    } else if (A.packed && A.stage_a) {
                         const uint32_t *p = reinterpret_cast<const uint32_t *>(A.idx) + o;
 #pragma unroll 4
                         for (int w = l; w < nt; w += tpo) {
@@ -329,10 +373,11 @@ __global__ void __launch_bounds__(256) astep_kernel(AStepArgs A) {
                             }
 #pragma unroll
                             for (int v = 0; v < V; ++v) {
-                                const T *sB = sBase + (size_t)v * A.smem_group;
-                                const T av = A.stage_a ? sB[A.aoff + ia]
+                                const T *sB = V > 1 ? sBase + v : sBase + (size_t)v * A.smem_group;
+                                const int64_t sv = V > 1 ? V : 1;
+                                const T av = A.stage_a ? sB[(A.aoff + ia) * sv]
                                                        : __ldg(reinterpret_cast<const T *>(A.ma) + (size_t)iv[v] * A.lda + ia);
-                                acc[v] += av * sB[ib];
+                                acc[v] += av * sB[ib * sv];
                             }
                         }
                     }
@@ -484,15 +529,23 @@ static int launch_astep_cfg(const AStepArgs &A0, void *stream) {
     const bool multi = A.comb == COMB_GENERAL && !A.top && A.nterms >= 8 && gt >= 32 && tune != 5 &&
                        (size_t)(256 / gt) * 4 * A.smem_group * sizeof(T) <= 200 * 1024;
     if constexpr (MODE != 0) {
-        if (multi && MODE == 2) {
-            if (nvec > 256) return launch_astep_t<T, RT, 256, 1, 16, 4, MODE>(A, stream);
-            return launch_astep_t<T, RT, 256, 1, 8, 4, MODE>(A, stream);
+        if constexpr (MODE == 2) {
+            if (multi) {
+                if (nvec > 256) return launch_astep_t<T, RT, 256, 1, 16, 4, MODE>(A, stream);
+                return launch_astep_t<T, RT, 256, 1, 8, 4, MODE>(A, stream);
+            }
         }
         if (nvec > 256) return launch_astep_t<T, RT, 256, 1, 16, 1, MODE>(A, stream);
         return launch_astep_gt<T, RT, 1, 8, MODE>(A, gt, stream);
     }
     if (multi) {
-        if (nvec > 256) return launch_astep_t<T, RT, 256, 1, 16, 4>(A, stream);
+        // V = 4 rows per group while they fit in ~100 KB (two CTAs per SM), else V = 2
+        const size_t per4 = (size_t)(256 / gt) * 4 * A.smem_group * sizeof(T);
+        if (nvec > 256) {
+            if (per4 > 100 * 1024 && tune != 6) return launch_astep_t<T, RT, 256, 1, 16, 2>(A, stream);
+            return launch_astep_t<T, RT, 256, 1, 16, 4>(A, stream);
+        }
+        if (per4 > 100 * 1024 && gt == 256 && tune != 6) return launch_astep_t<T, RT, 256, 1, 8, 2>(A, stream);
         switch (gt) {
             case 32: return launch_astep_t<T, RT, 32, 1, 8, 4>(A, stream);
             case 64: return launch_astep_t<T, RT, 64, 1, 8, 4>(A, stream);
