@@ -307,3 +307,24 @@ def test_fig1_analogue_treelet_distributions():
     within = max(D[0, 1], D[2, 3])
     between = min(D[0, 2], D[0, 3], D[1, 2], D[1, 3])
     assert between > within
+
+
+# --------------------------------------------------------------------------- table sharing / self steps
+SYMMETRIC = {
+    "spider3x2": [(0, 1), (1, 2), (0, 3), (3, 4), (0, 5), (5, 6)],          # 3 identical legs
+    "spider4x2": [(0, 1), (1, 2), (0, 3), (3, 4), (0, 5), (5, 6), (0, 7), (7, 8)],
+    "double_star": [(0, 1), (0, 2), (0, 3), (1, 4), (1, 5), (1, 6)],        # two isomorphic halves
+    "path9": [(i, i + 1) for i in range(8)],                                 # middle root: self top
+    "caterpillar": [(0, 1), (1, 2), (2, 3), (3, 4), (1, 5), (3, 6)],
+}
+
+
+@pytest.mark.parametrize("name", sorted(SYMMETRIC))
+def test_shared_and_self_steps_vs_oracle(oracle, name):
+    e = SYMMETRIC[name]
+    k = _k(e)
+    g = erdos_renyi(400, 2400, seed=k)
+    T = sg.template_build(k, e)
+    d = sg.plan_describe(G := _load(g), T, "u64")
+    assert len(d["steps"]) < k - 1 or any(s.get("self") for s in d["steps"]) or name == "caterpillar"
+    _check_all(oracle, g, e, [(3, 0), (3, 1)], roots=tuple(range(-1, k)), precs=("u64",))
