@@ -3,6 +3,7 @@
 // Alg. 5 and the estimate of Alg. 1.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cmath>
 #include <cstring>
 #include <mutex>
@@ -394,12 +395,12 @@ struct BatchLayout {
 
 static int64_t rup(int64_t x, int64_t m) { return (x + m - 1) / m * m; }
 
-static BatchLayout batch_layout(const std::vector<Plan *> &pls, int64_t n, int64_t nnz) {
+static BatchLayout batch_layout(const std::vector<Plan *> &pls, int64_t n, int64_t nnz, int64_t joint_tables = -1) {
     BatchLayout L;
     int64_t tables = 0, hist = 0;
     bool anch = false;
     for (Plan *p : pls) {
-        tables = std::max(tables, p->tables_bytes);
+        tables = std::max(tables, joint_tables >= 0 ? joint_tables : p->tables_bytes);
         hist = std::max(hist, p->hist_bytes);
         anch = anch || p->layout == LAYOUT_ANCHORED;
     }
@@ -414,6 +415,74 @@ static BatchLayout batch_layout(const std::vector<Plan *> &pls, int64_t n, int64
     L.off_results = off; off = rup(off + (int64_t)kResultsRing * 8 * (int64_t)std::max<size_t>(pls.size(), 1), 256);
     L.bytes = off;
     return L;
+}
+
+// Joint schedule of a batch: the templates' plans run in turn, and a rooted
+// sub-template class already computed for an earlier template (same canonical
+// string, e.g. the short paths and stars every treelet shares) is not recomputed
+// — its table stays live until its last consumer in any template.  The result is
+// one view Plan per template whose steps/buffers index a joint table arena.
+struct JointPlan {
+    std::vector<Plan> views;       // per template: steps to run + the joint buffer table
+    int64_t tables_bytes = 0;
+};
+
+static void joint_schedule(const std::vector<Plan *> &pls, JointPlan &J) {
+    std::vector<Buffer> bufs;
+    std::map<std::string, int> class_buf, uses;
+    for (Plan *p : pls)
+        for (const Step &st : p->steps) {
+            if (!st.self_a) uses[st.canon_a]++;
+            uses[st.canon_p]++;
+        }
+    std::vector<std::pair<int64_t, int64_t>> live;
+    int64_t arena = 0;
+    auto alloc = [&](int64_t bytes) -> int64_t {
+        int64_t pos = 0;
+        std::sort(live.begin(), live.end());
+        for (auto &iv : live) {
+            if (iv.first - pos >= bytes) break;
+            pos = std::max(pos, rup(iv.first + iv.second, 256));
+        }
+        live.push_back({pos, bytes});
+        arena = std::max(arena, pos + bytes);
+        return pos;
+    };
+    auto release = [&](int b) {
+        if (b < 0) return;
+        for (size_t q = 0; q < live.size(); ++q)
+            if (live[q].first == bufs[b].offset) { live.erase(live.begin() + q); break; }
+    };
+    J.views.clear();
+    for (Plan *p : pls) {
+        Plan v = *p;  // copies index offsets; d_index stays owned by p
+        v.steps.clear();
+        for (const Step &st0 : p->steps) {
+            Step st = st0;
+            const bool have = !st.top && class_buf.count(st.canon_out);
+            if (have) {  // computed by an earlier template: only release bookkeeping
+                if (!st.self_a && --uses[st.canon_a] == 0) release(class_buf[st.canon_a]);
+                if (--uses[st.canon_p] == 0) release(class_buf[st.canon_p]);
+                continue;
+            }
+            st.buf_a = (!st.self_a && class_buf.count(st.canon_a)) ? class_buf[st.canon_a] : -1;
+            st.buf_p = class_buf.count(st.canon_p) ? class_buf[st.canon_p] : -1;
+            if (!st.top) {
+                Buffer b;
+                b.bytes = st0.buf_out >= 0 ? p->bufs[st0.buf_out].bytes : 0;
+                b.offset = alloc(b.bytes);
+                bufs.push_back(b);
+                st.buf_out = (int)bufs.size() - 1;
+                class_buf[st.canon_out] = st.buf_out;
+            }
+            if (!st.self_a && --uses[st.canon_a] == 0) release(st.buf_a);
+            if (--uses[st.canon_p] == 0) release(st.buf_p);
+            v.steps.push_back(st);
+        }
+        J.views.push_back(std::move(v));
+    }
+    for (Plan &v : J.views) v.bufs = bufs;
+    J.tables_bytes = rup(arena, 256);
 }
 
 static sg2v_status batch_plans(const sg2v_graph *g, const sg2v_template *const *ts, int32_t m, sg2v_precision prec,
@@ -660,7 +729,9 @@ static sg2v_status count_core(const sg2v_graph *g, const sg2v_template *const *t
         std::vector<Plan *> pls;
         st = batch_plans(g, ts, m, o.precision, o.layout, true, o.mem_budget_bytes, pls);
         if (st != SG2V_OK) return st;
-        const BatchLayout L = batch_layout(pls, g->n, g->nnz);
+        JointPlan J;
+        if (pls.size() > 1) joint_schedule(pls, J);
+        const BatchLayout L = batch_layout(pls, g->n, g->nnz, pls.size() > 1 ? J.tables_bytes : -1);
         char *ws = (char *)o.workspace;
         bool own = false;
         if (ws) {
@@ -706,7 +777,7 @@ static sg2v_status count_core(const sg2v_graph *g, const sg2v_template *const *t
             if (need_hist && (rc = launch_hist(*g, *pls[0], colors, H, s))) return cuda_fail("hist", rc);
             if (anch && (rc = launch_bucket(*g, *pls[0], colors, hcnt, bcol, s))) return cuda_fail("bucket", rc);
             for (int32_t tq = 0; tq < m; ++tq) {
-                const Plan *pl = pls[tq];
+                const Plan *pl = pls.size() > 1 ? &J.views[tq] : pls[tq];
                 for (const Step &stp : pl->steps) {
                     rc = anch ? launch_astep(*g, *pl, stp, colors, hcnt, bcol, ws, rowval, s)
                               : launch_step(*g, *pl, stp, colors, H, ws, rowval, s);
@@ -787,7 +858,9 @@ sg2v_status sg2v_workspace_bytes_batch(const sg2v_graph *g, const sg2v_template 
     std::vector<Plan *> pls;
     sg2v_status st = batch_plans(g, templates, m, prec, tls_layout(), false, tls_budget(), pls);
     if (st != SG2V_OK) return st;
-    *bytes = pls.empty() ? 0 : (uint64_t)batch_layout(pls, g->n, g->nnz).bytes;
+    JointPlan J;
+    if (pls.size() > 1) joint_schedule(pls, J);
+    *bytes = pls.empty() ? 0 : (uint64_t)batch_layout(pls, g->n, g->nnz, pls.size() > 1 ? J.tables_bytes : -1).bytes;
     return SG2V_OK;
 }
 

@@ -365,6 +365,9 @@ static bool plan_chain(const Template &t, const Chain &c, int root, int64_t n, i
         st.ldp = (st.src == SRC_HIST) ? round_up(k, vn) : round_up(st.cp, vn);
         st.ldb = anch ? round_up(st.cb, vn) : st.ldp;
         st.self_a = self_step(v);
+        st.canon_out = canon[v];
+        st.canon_a = canon[nd.active];
+        st.canon_p = canon[nd.passive];
         st.buf_a = (!st.self_a && class_buf.count(canon[nd.active])) ? class_buf[canon[nd.active]] : -1;
         st.buf_p = class_buf.count(canon[nd.passive]) ? class_buf[canon[nd.passive]] : -1;
         if (st.src == SRC_HIST && !anch) pl.need_hist = true;

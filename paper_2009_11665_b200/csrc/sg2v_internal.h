@@ -69,6 +69,7 @@ struct Step {
     int64_t nterms = 0;                    // splits per output (GENERAL)
     int packed = 0;                        // anchored GENERAL: pairs packed ia | ip << 16, term-major
     bool self_a = false;                   // anchored: T_s = root + 2 copies of X, M_a(i,·) = B(i,·)
+    std::string canon_out, canon_a, canon_p;  // rooted classes of T_s, T_a, T_p (table sharing)
     int gt = 32;                           // threads per row group (step kernel)
     double alg_bytes = 0.0;                // algorithmic HBM bytes
     double ema_terms = 0.0;
