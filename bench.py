@@ -43,7 +43,7 @@ def _args():
     p.add_argument("--impl", default="sg2v", choices=["sg2v", "reference"])
     p.add_argument("--template", default="u15-1")
     p.add_argument("--precision", default="f32", choices=["f32", "f64", "u64"])
-    p.add_argument("--layout", default="anchored", choices=["anchored", "dense"])
+    p.add_argument("--layout", default="anchored", choices=["anchored", "anchored_plain", "dense"])
     p.add_argument("--scale", type=int, default=20)
     p.add_argument("--seed", type=int, default=1)
     p.add_argument("--no-cpu-baseline", action="store_true")

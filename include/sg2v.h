@@ -119,8 +119,16 @@ typedef struct {
                                  F32/F64, uint64 for U64)                            */
     int32_t layout;           /* count-table layout: 0 = root-colour anchored
                                  (default; rows hold only colour sets containing
-                                 c(i), C(k-1,s-1) columns),
-                                 1 = dense n x C(k,s) as in P:227.  Same results. */
+                                 c(i), C(k-1,s-1) columns), where
+                                 the planner may store a table read only as a
+                                 passive child as k-1 per-consumer-colour segments
+                                 of C(k-2,s-1) sets ("exclusion-projected", more
+                                 memory, fewer gathered bytes),
+                                 1 = dense n x C(k,s) as in P:227,
+                                 2 = anchored without projected tables,
+                                 3 = anchored with every eligible table projected
+                                     (as far as the budget allows; tests).
+                                 Same results in every layout. */
 } sg2v_options;
 
 void sg2v_options_default(sg2v_options *o);

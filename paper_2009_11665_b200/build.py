@@ -38,15 +38,27 @@ def build(force: bool = False, verbose: bool = False) -> str:
         return LIB
     os.makedirs(LIBDIR, exist_ok=True)
     cuda_lib = "/usr/local/cuda/lib64"
-    cmd = [nvcc(), "-O3", "-std=c++17", "-shared", "-Xcompiler", "-fPIC,-O3",
-           "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo",
-           "-cudart", "shared", "-Xlinker", f"-rpath,{cuda_lib}", "-ldl",
-           "-I", os.path.join(ROOT, "include"),
-           "-o", LIB] + [os.path.join(CSRC, s) for s in SOURCES]
+    common = [nvcc(), "-O3", "-std=c++17", "-Xcompiler", "-fPIC,-O3",
+              "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo",
+              "-I", os.path.join(ROOT, "include")]
     if verbose:
-        cmd.insert(1, "-Xptxas=-v")
-        print(" ".join(cmd))
-    subprocess.check_call(cmd)
+        common.insert(1, "-Xptxas=-v")
+    objdir = os.path.join(LIBDIR, "obj")
+    os.makedirs(objdir, exist_ok=True)
+    objs, procs = [], []
+    for s in SOURCES:  # one nvcc per translation unit, in parallel
+        o = os.path.join(objdir, s + ".o")
+        objs.append(o)
+        cmd = common + ["-c", os.path.join(CSRC, s), "-o", o]
+        if verbose:
+            print(" ".join(cmd))
+        procs.append((cmd, subprocess.Popen(cmd)))
+    for cmd, pr in procs:
+        if pr.wait() != 0:
+            raise subprocess.CalledProcessError(pr.returncode, cmd)
+    link = [nvcc(), "-shared", "-gencode", "arch=compute_100a,code=sm_100a", "-cudart", "shared",
+            "-Xlinker", f"-rpath,{cuda_lib}", "-ldl", "-o", LIB] + objs
+    subprocess.check_call(link)
     return LIB
 
 

@@ -98,6 +98,12 @@ struct AStepArgs {
     int64_t ldp, cp;    // its row stride / width C(k-1,p-1)
     int src_hist;       // p = 1: B(i,{y}) = H(i,y)
     const int32_t *pmap;  // push map [x][c(i)][cp] -> B column or -1
+    int64_t ldseg_p;    // > 0: the passive table is exclusion-projected: k-1 segments of
+                        //   ldseg_p elements per row, segment y' = sets avoiding colour y
+    int64_t ldseg_out;  // > 0: write the output table exclusion-projected (stride lds)
+    const int32_t *omap;  // its write map (leaf-active: inverse [y'][ldseg_out]; general:
+                          //   forward [o][k-1] -> position in segment y', or -1)
+    int64_t ocols;      // eMA outputs per row, padded to 16 B
     const char *ma;     // active anchored table (GENERAL)
     int64_t lda;
     char *ms;           // output table (non-top)
@@ -131,7 +137,7 @@ __device__ __forceinline__ void gather_row(const AStepArgs &A, int64_t i, int ci
                                            uint64_t pol_last, uint64_t pol_first) {
     constexpr int VN = Vec<T>::N;
     constexpr int32_t kIdMask = (1 << kClassShift) - 1;
-    const int64_t nvec_p = A.ldp / VN;
+    const int64_t nvec_p = (A.ldseg_p > 0 ? A.ldseg_p : A.ldp) / VN;
     const size_t row_bytes = (size_t)A.ldp * sizeof(T);
     const int k = A.k;
     const int32_t *h = A.hcnt + (size_t)i * A.kp;
@@ -143,11 +149,19 @@ __device__ __forceinline__ void gather_row(const AStepArgs &A, int64_t i, int ci
     for (int x = 0; x < k; ++x) {
         const int cnt = __ldg(h + x);
         if (x != ci && cnt > 0) {
+            const int r = ci - (ci > x ? 1 : 0);  // c(i)'s element in x's universe [k-1]
             const int32_t *mp = A.pmap + ((size_t)x * k + ci) * A.cp_map + A.u0;
+            // byte offset of this lane's vector in a neighbour row; a projected source
+            // is read in segment r (the sets avoiding c(i))
+            const int64_t sbase = (A.ldseg_p > 0 ? (int64_t)r * A.ldseg_p * (int64_t)sizeof(T) : 0) + (int64_t)t * 16;
             for (int64_t v0 = 0; v0 < nvec_p; v0 += GT * R) {
                 uint4 acc[R];
+                bool need[R];
 #pragma unroll
-                for (int q = 0; q < R; ++q) acc[q] = make_uint4(0, 0, 0, 0);
+                for (int q = 0; q < R; ++q) {
+                    acc[q] = make_uint4(0, 0, 0, 0);
+                    need[q] = v0 + q * GT + t < nvec_p;
+                }
                 int64_t e2 = e;
                 const int64_t e3 = e + cnt;
                 for (; e2 + U <= e3; e2 += U) {
@@ -165,9 +179,9 @@ __device__ __forceinline__ void gather_row(const AStepArgs &A, int64_t i, int ci
 #pragma unroll
                         for (int q = 0; q < R; ++q) {
                             const int64_t v = v0 + q * GT + t;
-                            const char *src = A.mp + (size_t)jj[u] * row_bytes + v * 16;
-                            xv[u][q] = (v < nvec_p) ? (A.hint ? ldg16_pol(src, pol[u]) : ldg16(src))
-                                                    : make_uint4(0, 0, 0, 0);
+                            const char *src = A.mp + (size_t)jj[u] * row_bytes + sbase + (v - t) * 16;
+                            xv[u][q] = need[q] ? (A.hint ? ldg16_pol(src, pol[u]) : ldg16(src))
+                                               : make_uint4(0, 0, 0, 0);
                         }
 #pragma unroll
                     for (int u = 0; u < U; ++u)
@@ -189,8 +203,8 @@ __device__ __forceinline__ void gather_row(const AStepArgs &A, int64_t i, int ci
 #pragma unroll
                             for (int q = 0; q < R; ++q) {
                                 const int64_t v = v0 + q * GT + t;
-                                xv[u][q] = (jj[u] >= 0 && v < nvec_p) ? ldg16(A.mp + (size_t)jj[u] * row_bytes + v * 16)
-                                                                      : make_uint4(0, 0, 0, 0);
+                                xv[u][q] = (jj[u] >= 0 && need[q]) ? ldg16(A.mp + (size_t)jj[u] * row_bytes + sbase + (v - t) * 16)
+                                                                   : make_uint4(0, 0, 0, 0);
                             }
 #pragma unroll
                         for (int u = 0; u < UT; ++u)
@@ -202,7 +216,7 @@ __device__ __forceinline__ void gather_row(const AStepArgs &A, int64_t i, int ci
 #pragma unroll
                 for (int q = 0; q < R; ++q) {
                     const int64_t v = v0 + q * GT + t;
-                    if (v < nvec_p) {
+                    if (need[q]) {
 #pragma unroll
                         for (int el = 0; el < VN; ++el) {
                             const int64_t u = v * VN + el;
@@ -314,14 +328,27 @@ __global__ void __launch_bounds__(256) astep_kernel(AStepArgs A) {
                 if (actv[v]) {
                     T *out = reinterpret_cast<T *>(A.ms) + (size_t)iv[v] * A.lds;
                     const T *sB = sBase + (size_t)v * A.smem_group;
-                    for (int64_t q = t; q < A.lds / VN; q += GT)
-                        reinterpret_cast<uint4 *>(out)[q] = reinterpret_cast<const uint4 *>(sB)[q];
+                    if (A.ldseg_out > 0) {
+                        // projected: segment y' position u <- B(i, omap[y'][u]) (16-B stores)
+                        for (int64_t q = t; q < A.lds / VN; q += GT) {
+                            uint4 w;
+#pragma unroll
+                            for (int el = 0; el < VN; ++el) {
+                                const int32_t c = __ldg(A.omap + q * VN + el);
+                                vset<T>(w, el, c >= 0 ? sB[c] : (T)0);
+                            }
+                            reinterpret_cast<uint4 *>(out)[q] = w;
+                        }
+                    } else {
+                        for (int64_t q = t; q < A.lds / VN; q += GT)
+                            reinterpret_cast<uint4 *>(out)[q] = reinterpret_cast<const uint4 *>(sB)[q];
+                    }
                 }
         } else if (!A.top) {
             // split table term-major: entry (w, o) at w*cs + o, so the lanes (consecutive
             // outputs o) read consecutive words; each entry serves the group's V rows.
             // With few outputs (cs < GT) tpo consecutive lanes share an output.
-            const int tpo = A.tpo, cs = (int)A.cs, nt = (int)A.nterms, lds = (int)A.lds;
+            const int tpo = A.tpo, cs = (int)A.cs, nt = (int)A.nterms, lds = (int)A.ocols;
             const int l = t % tpo;
             for (int ob = 0; ob < lds; ob += GT / tpo) {
                 const int o = ob + t / tpo;
@@ -389,8 +416,18 @@ __global__ void __launch_bounds__(256) astep_kernel(AStepArgs A) {
                         for (int off = 16; off > 0; off >>= 1)
                             if (off < tpo) acc[v] += __shfl_xor_sync(0xffffffffu, acc[v], off);
                     }
-                    if (actv[v] && l == 0 && o < lds)
-                        reinterpret_cast<T *>(A.ms)[(size_t)iv[v] * A.lds + o] = acc[v];
+                    if (actv[v] && l == 0 && o < lds) {
+                        T *orow = reinterpret_cast<T *>(A.ms) + (size_t)iv[v] * A.lds;
+                        if (A.ldseg_out > 0) {  // projected: every segment y' ∌ o
+                            if (o < cs)
+                                for (int y = 0; y < A.k - 1; ++y) {
+                                    const int32_t pos = __ldg(A.omap + (size_t)o * (A.k - 1) + y);
+                                    if (pos >= 0) orow[(size_t)y * A.ldseg_out + pos] = acc[v];
+                                }
+                        } else {
+                            orow[o] = acc[v];
+                        }
+                    }
                 }
             }
         } else if (actv[0]) {
@@ -515,8 +552,10 @@ static int launch_astep_cfg(const AStepArgs &A0, void *stream) {
         const char *e = getenv("SG2V_TUNE");
         tune = e ? atoi(e) : 0;
     }
-    const int64_t nvec = A.src_hist ? 1 : A.ldp / VN;
-    const int64_t nout = std::max(A.ldb, A.lds) / VN;
+    const int64_t nvec = A.src_hist ? 1 : (A.ldseg_p > 0 ? A.ldseg_p : A.ldp) / VN;
+    // (a projected output row is written by the same lanes in more passes: the group
+    // is sized by the gather and the eMA, not by the k-1 output segments)
+    const int64_t nout = std::max(A.ldb, A.ocols) / VN;
     int64_t want = std::max<int64_t>(nvec, (nout + 3) / 4);
     int gt = 4;
     while (gt < want && gt < 256) gt *= 2;
@@ -610,6 +649,10 @@ int launch_astep_vp(const Graph &g, const Plan &pl, const Step &st, const uint8_
     A.ms = st.top ? nullptr : tables + pl.bufs[st.buf_out].offset;
     A.lds = st.lds;
     A.cs = st.cs;
+    A.ldseg_p = st.proj_p ? st.ldseg_p : 0;
+    A.ldseg_out = st.proj_out ? st.ldseg_out : 0;
+    A.omap = st.omap_off >= 0 ? pl.d_index + st.omap_off : nullptr;
+    A.ocols = st.top ? 1 : (st.cs + (16 / pl.elem) - 1) / (16 / pl.elem) * (16 / pl.elem);
     A.ldb = st.ldb;
     A.cb = st.cb;
     A.comb = st.comb;

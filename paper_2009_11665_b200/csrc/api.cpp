@@ -183,13 +183,18 @@ static uint64_t tls_budget() { return g_opts_init ? g_opts.mem_budget_bytes : 0;
 
 static sg2v_status get_plan(int64_t n, int64_t nnz, int device, const Template &t, sg2v_precision prec,
                             int32_t layout, bool upload, Plan **out, uint64_t explicit_budget = 0) {
-    if (layout != 0 && layout != 1) { set_error("layout must be 0 (anchored) or 1 (dense)"); return SG2V_EINVAL; }
+    if (layout < 0 || layout > 3) {
+        set_error("layout must be 0 (anchored), 1 (dense), 2 (anchored, no projected tables) or 3 (anchored, "
+                  "every eligible table projected)");
+        return SG2V_EINVAL;
+    }
     const uint64_t budget = plan_budget(explicit_budget, device);
     auto key = std::make_tuple((int)prec, n, nnz, device, (int)layout, budget);
     auto &slot = const_cast<Template &>(t).plans[key];
     if (!slot) {
         std::unique_ptr<Plan> pl;
-        sg2v_status st = make_plan(t, n, nnz, prec, current_layout(layout), budget, pl);
+        sg2v_status st = make_plan(t, n, nnz, prec, current_layout(layout), budget, pl, 0, 0,
+                                   layout == 0 ? 1 : layout == 3 ? 2 : 0);
         if (st != SG2V_OK) return st;
         slot = std::move(pl);
     }
@@ -345,14 +350,23 @@ sg2v_status sg2v_workspace_bytes(const sg2v_graph *g, const sg2v_template *t, sg
     return SG2V_OK;
 }
 
+static sg2v_status plan_describe_dev(int64_t n, int64_t nnz, int device, const sg2v_template *t,
+                                     sg2v_precision prec, char *buf, uint64_t buf_len, uint64_t *needed);
+
 sg2v_status sg2v_plan_describe(const sg2v_graph *g, const sg2v_template *t, sg2v_precision prec, char *buf,
                                uint64_t buf_len, uint64_t *needed) {
     if (!g) { set_error("NULL argument"); return SG2V_EINVAL; }
-    return sg2v_plan_describe_n(g->n, g->nnz, t, prec, buf, buf_len, needed);
+    // the plan sg2v_count will use on g's device (its memory budget)
+    return plan_describe_dev(g->n, g->nnz, g->device, t, prec, buf, buf_len, needed);
 }
 
 sg2v_status sg2v_plan_describe_n(int64_t n, int64_t nnz, const sg2v_template *t, sg2v_precision prec, char *buf,
                                  uint64_t buf_len, uint64_t *needed) {
+    return plan_describe_dev(n, nnz, -1, t, prec, buf, buf_len, needed);
+}
+
+static sg2v_status plan_describe_dev(int64_t n, int64_t nnz, int device, const sg2v_template *t,
+                                     sg2v_precision prec, char *buf, uint64_t buf_len, uint64_t *needed) {
     if (!t || n < 0 || nnz < 0) { set_error("bad argument"); return SG2V_EINVAL; }
     if (prec < SG2V_F32 || prec > SG2V_U64) { set_error("bad precision"); return SG2V_EINVAL; }
     std::string s;
@@ -360,7 +374,7 @@ sg2v_status sg2v_plan_describe_n(int64_t n, int64_t nnz, const sg2v_template *t,
         s = "{\"k\":" + std::to_string(t->k) + ",\"steps\":[],\"workspace_bytes\":0,\"alg_bytes\":0}";
     } else {
         Plan *pl = nullptr;
-        sg2v_status st = get_plan(n, nnz, -1, *t, prec, tls_layout(), false, &pl, tls_budget());
+        sg2v_status st = get_plan(n, nnz, device, *t, prec, tls_layout(), false, &pl, tls_budget());
         if (st != SG2V_OK) return st;
         s = pl->describe();
     }
@@ -491,7 +505,10 @@ static sg2v_status batch_plans(const sg2v_graph *g, const sg2v_template *const *
     for (int32_t q = 0; q < m; ++q) {
         if (ts[q]->k == 1 || g->n == 0) continue;
         Plan *pl = nullptr;
-        sg2v_status st = get_plan(g->n, g->nnz, g->device, *ts[q], prec, layout, upload, &pl, budget);
+        // a joint schedule of several templates shares tables across them: plain
+        // anchored rows only (a single template may use exclusion-projected tables)
+        sg2v_status st = get_plan(g->n, g->nnz, g->device, *ts[q], prec, (layout == 0 || layout == 3) && m > 1 ? 2 : layout, upload,
+                                  &pl, budget);
         if (st != SG2V_OK) return st;
         pls.push_back(pl);
     }
@@ -536,7 +553,7 @@ static sg2v_status count_vp(const sg2v_graph *g, const sg2v_template *t, int32_t
                             sg2v_options o, double *estimate, double *colorful_out, uint64_t *colorful_u64_out) {
     sg2v_comm *c = (sg2v_comm *)o.nccl_comm;
     if (!c) { set_error("mode 1 needs options.nccl_comm (sg2v_comm_init_*)"); return SG2V_EINVAL; }
-    if (o.layout != 0) { set_error("the vertex-partitioned mode uses the anchored layout"); return SG2V_EINVAL; }
+    if (o.layout == 1) { set_error("the vertex-partitioned mode uses the anchored layout"); return SG2V_EINVAL; }
     const int64_t n_global = g->partitioned ? g->n_global : g->n;
     const int64_t nl = (n_global + c->world - 1) / c->world;
     const int64_t begin = g->partitioned ? g->row_begin : 0;
@@ -564,7 +581,7 @@ static sg2v_status count_vp(const sg2v_graph *g, const sg2v_template *t, int32_t
         if (!slot) {
             std::unique_ptr<Plan> pl;
             st = make_plan(*t, std::max<int64_t>(g->n, 1), std::max<int64_t>(g->nnz, 1), o.precision, LAYOUT_ANCHORED,
-                           0, pl, (int64_t)c->world * nl, o.col_tile);
+                           0, pl, (int64_t)c->world * nl, o.col_tile, 0);
             if (st != SG2V_OK) return st;
             slot = std::move(pl);
         }

@@ -114,6 +114,12 @@ __device__ __forceinline__ T vget(const uint4 &v, int e) {
     return reinterpret_cast<const T *>(&v)[e];
 }
 
+// set element e (0..VN-1) of a 16-B vector
+template <typename T>
+__device__ __forceinline__ void vset(uint4 &v, int e, T x) {
+    reinterpret_cast<T *>(&v)[e] = x;
+}
+
 int num_sms();
 
 }  // namespace sg2v

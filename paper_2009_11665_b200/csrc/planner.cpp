@@ -216,9 +216,10 @@ static int64_t table_width(Layout L, int k, int size) {
 
 // Build steps, schedule, buffers and the model for one chain.
 static bool plan_chain(const Template &t, const Chain &c, int root, int64_t n, int64_t nnz,
-                       sg2v_precision prec, Layout L, Plan &pl) {
+                       sg2v_precision prec, Layout L, Plan &pl, const std::set<std::string> &proj = {}) {
     const int k = t.k;
     pl = Plan();
+    pl.proj = proj;
     pl.k = k;
     pl.root = root;
     pl.prec = prec;
@@ -236,6 +237,27 @@ static bool plan_chain(const Template &t, const Chain &c, int root, int64_t n, i
         const Node &nd = pl.nodes[i];
         if (nd.active >= 0 && (int)i != c.top)
             out_bytes[i] = n * round_up(table_width(L, k, nd.size), vn) * pl.elem;
+    }
+    // canonical strings first (projected classes change the table sizes)
+    std::vector<std::string> canon(pl.nodes.size());
+    {
+        std::vector<std::vector<std::string>> kids(pl.nodes.size());
+        for (size_t v = 0; v < pl.nodes.size(); ++v) {  // children precede parents
+            const Node &nd = pl.nodes[v];
+            if (nd.active >= 0) {
+                kids[v] = kids[nd.active];
+                kids[v].push_back(canon[nd.passive]);
+                std::sort(kids[v].begin(), kids[v].end());
+            }
+            std::string cs = "(";
+            for (auto &x : kids[v]) cs += x;
+            canon[v] = cs + ")";
+        }
+    }
+    for (size_t i = 0; i < pl.nodes.size(); ++i) {
+        const Node &nd = pl.nodes[i];
+        if (nd.active >= 0 && (int)i != c.top && proj.count(canon[i]))
+            out_bytes[i] = n * (int64_t)(k - 1) * round_up(binom(k - 2, nd.size - 1), vn) * pl.elem;
     }
     std::vector<int> sched;
     std::function<int64_t(int, std::vector<int> &)> order = [&](int v, std::vector<int> &seq) -> int64_t {
@@ -266,22 +288,8 @@ static bool plan_chain(const Template &t, const Chain &c, int root, int64_t n, i
     // its root at i, so it depends only on T_s's rooted isomorphism
     // class: compute each class once (e.g. the two arms of a path rooted at its
     // middle) and let every parent read it.  canon(node) = AHU string of the
-    // rooted sub-template (children multiset, sorted).
-    std::vector<std::string> canon(pl.nodes.size());
-    {
-        std::vector<std::vector<std::string>> kids(pl.nodes.size());
-        for (size_t v = 0; v < pl.nodes.size(); ++v) {  // children precede parents
-            const Node &nd = pl.nodes[v];
-            if (nd.active >= 0) {
-                kids[v] = kids[nd.active];
-                kids[v].push_back(canon[nd.passive]);
-                std::sort(kids[v].begin(), kids[v].end());
-            }
-            std::string cs = "(";
-            for (auto &x : kids[v]) cs += x;
-            canon[v] = cs + ")";
-        }
-    }
+    // rooted sub-template (children multiset, sorted; computed above).
+    //
     // Self steps (anchored): T_s = root ρ + two isomorphic child subtrees X, split as
     // active = ρ + X (itself leaf-active over X) and passive = X.  The active row is
     // M_a(i,·) = B_X(i,·) with the same [k-1]-subset indexing as the step's own
@@ -316,11 +324,34 @@ static bool plan_chain(const Template &t, const Chain &c, int root, int64_t n, i
         };
         visit(c.top);
     }
+    // Exclusion-projected tables: a class read only as the PASSIVE side of row-streaming
+    // gathers may be stored as k-1 segments per row, one per consumer colour y ≠ c(i),
+    // holding the sets that avoid y (C(k-2,s-1) entries): a consumer of colour c(i)
+    // streams exactly the sets it can use instead of the whole C(k-1,s-1) row (where
+    // a fraction (s-1)/(k-1) contain c(i) and are discarded), for k-s times the table
+    // memory.  The planner picks the classes (make_plan).
+    {
+        std::map<std::string, bool> ok;
+        for (int v : sched) {
+            const Node &nd = pl.nodes[v];
+            const bool top = (v == c.top);
+            const int a = pl.nodes[nd.active].size, p = pl.nodes[nd.passive].size;
+            if (!self_step(v) && a > 1) ok[canon[nd.active]] = false;  // read as M_a
+            if (p > 1) {
+                const bool top_leaf = top && a == 1;                   // one column per edge
+                auto it = ok.find(canon[nd.passive]);
+                ok[canon[nd.passive]] = (it == ok.end() || it->second) && !top_leaf && anch;
+            }
+        }
+        for (auto &kv : ok)
+            if (kv.second) pl.proj_cands.push_back(kv.first);
+    }
+    auto key = [&](int v) { return proj.count(canon[v]) ? canon[v] + "|x" : canon[v]; };
     // uses of each class by the scheduled steps (a table is freed after its last use)
     std::map<std::string, int> uses;
     for (int v : sched) {
-        if (!self_step(v)) uses[canon[pl.nodes[v].active]]++;
-        uses[canon[pl.nodes[v].passive]]++;
+        if (!self_step(v)) uses[key(pl.nodes[v].active)]++;
+        uses[key(pl.nodes[v].passive)]++;
     }
 
     // --- first-fit arena over the schedule ---
@@ -360,16 +391,27 @@ static bool plan_chain(const Template &t, const Chain &c, int root, int64_t n, i
         st.ca = table_width(L, k, st.a);
         st.cp = table_width(L, k, st.p);
         st.cb = anch ? binom(k - 1, st.p) : st.cp;
+        st.proj_out = !st.top && proj.count(canon[v]);
+        st.proj_p = st.src == SRC_GATHER && proj.count(canon[nd.passive]);
         st.lds = st.top ? 1 : round_up(st.cs, vn);
+        if (st.proj_out) {
+            st.ldseg_out = round_up(binom(k - 2, st.s - 1), vn);
+            st.lds = (int64_t)(k - 1) * st.ldseg_out;
+        }
         st.lda = round_up(st.ca, vn);
         st.ldp = (st.src == SRC_HIST) ? round_up(k, vn) : round_up(st.cp, vn);
+        if (st.proj_p) {  // gather width: one segment
+            st.cp = binom(k - 2, st.p - 1);
+            st.ldseg_p = round_up(st.cp, vn);
+            st.ldp = (int64_t)(k - 1) * st.ldseg_p;
+        }
         st.ldb = anch ? round_up(st.cb, vn) : st.ldp;
         st.self_a = self_step(v);
-        st.canon_out = canon[v];
-        st.canon_a = canon[nd.active];
-        st.canon_p = canon[nd.passive];
-        st.buf_a = (!st.self_a && class_buf.count(canon[nd.active])) ? class_buf[canon[nd.active]] : -1;
-        st.buf_p = class_buf.count(canon[nd.passive]) ? class_buf[canon[nd.passive]] : -1;
+        st.canon_out = key(v);
+        st.canon_a = key(nd.active);
+        st.canon_p = key(nd.passive);
+        st.buf_a = (!st.self_a && class_buf.count(st.canon_a)) ? class_buf[st.canon_a] : -1;
+        st.buf_p = class_buf.count(st.canon_p) ? class_buf[st.canon_p] : -1;
         if (st.src == SRC_HIST && !anch) pl.need_hist = true;
         if (!st.top) {
             Buffer b;
@@ -378,10 +420,10 @@ static bool plan_chain(const Template &t, const Chain &c, int root, int64_t n, i
             pl.bufs.push_back(b);
             st.buf_out = (int)pl.bufs.size() - 1;
             node_buf[v] = st.buf_out;
-            class_buf[canon[v]] = st.buf_out;
+            class_buf[st.canon_out] = st.buf_out;
         }
-        if (!st.self_a && --uses[canon[nd.active]] == 0) release(st.buf_a);
-        if (--uses[canon[nd.passive]] == 0) release(st.buf_p);
+        if (!st.self_a && --uses[st.canon_a] == 0) release(st.buf_a);
+        if (--uses[st.canon_p] == 0) release(st.buf_p);
 
         // algorithmic bytes (useful columns only) and the model (sector-rounded)
         double bytes = 0.0, mbytes = 0.0;
@@ -402,7 +444,7 @@ static bool plan_chain(const Template &t, const Chain &c, int root, int64_t n, i
                             ? nnz * 4.0 + nnz * live_frac * (double)round_up(st.cp * pl.elem, 32) + n * 12.0
                             : hsrc;
             double ma = (st.comb == COMB_GENERAL && !st.self_a) ? n * (double)st.ca * E : n * 1.0;
-            double w = st.top ? n * 8.0 : n * (double)st.cs * E;
+            double w = st.top ? n * 8.0 : st.proj_out ? n * (double)st.lds * E : n * (double)st.cs * E;
             bytes = gather + ma + w;
             mbytes = mg + ma + w;
             if (anch && st.src == SRC_GATHER)  // per-row push of k-1 colour partial sums through smem
@@ -459,9 +501,52 @@ static bool build_index(Plan &pl) {
     pl.index.clear();
     auto align = [&]() { while (pl.index.size() % 4) pl.index.push_back(0); };
     std::map<int, int64_t> push_maps;               // anchored push map per passive size p
+    std::map<int, int64_t> push_maps_x;             // ... for exclusion-projected sources
     for (Step &st : pl.steps) {
-        // ---- anchored gather: push map [x][ci][u] -> B column (or -1) ----
-        if (anch && st.src == SRC_GATHER && (pl.vp || !(st.top && st.comb == COMB_ACTIVE_LEAF))) {
+        // ---- projected output: write map ----
+        if (st.proj_out) {
+            const int m = st.s - 1;  // stored sets: (s-1)-subsets of [k-1] (i's universe)
+            align();
+            st.omap_off = (int64_t)pl.index.size();
+            if (st.comb == COMB_ACTIVE_LEAF) {
+                // inverse: segment y', position u -> column of B(i,·) (= M_s(i,·)), -1 = pad
+                std::vector<uint32_t> us;
+                for_each_subset(k - 2, m, [&](uint32_t x) { us.push_back(x); });
+                for (int y = 0; y < k - 1; ++y)
+                    for (int64_t u = 0; u < st.ldseg_out; ++u)
+                        pl.index.push_back(u < (int64_t)us.size() ? (int32_t)colex_rank(insert_gap(us[(size_t)u], y)) : -1);
+            } else {
+                // forward: output o, segment y' -> position in the segment, -1 if o ∋ y'
+                for_each_subset(k - 1, m, [&](uint32_t S) {
+                    for (int y = 0; y < k - 1; ++y)
+                        pl.index.push_back((S >> y & 1u) ? -1 : (int32_t)colex_rank(drop_bit(S, y)));
+                });
+            }
+        }
+        // ---- anchored gather from a projected table: push map [x][ci][u] -> B column ----
+        if (st.proj_p) {
+            auto it = push_maps_x.find(st.p);
+            if (it != push_maps_x.end()) {
+                st.map_off = it->second;
+            } else {
+                align();
+                st.map_off = (int64_t)pl.index.size();
+                std::vector<uint32_t> us;  // (p-1)-subsets of [k] \ {x, ci}, relabelled into [k-2]
+                for_each_subset(k - 2, st.p - 1, [&](uint32_t m) { us.push_back(m); });
+                for (int x = 0; x < k; ++x)
+                    for (int ci = 0; ci < k; ++ci)
+                        for (uint32_t u : us) {
+                            int32_t tcol = -1;
+                            if (x != ci) {
+                                const int lo = std::min(x, ci), hi = std::max(x, ci);
+                                const uint32_t U = insert_gap(insert_gap(u, lo), hi);  // subset of [k] \ {x, ci}
+                                tcol = (int32_t)colex_rank(drop_bit(U | (1u << x), ci));
+                            }
+                            pl.index.push_back(tcol);
+                        }
+                push_maps_x[st.p] = st.map_off;
+            }
+        } else if (anch && st.src == SRC_GATHER && (pl.vp || !(st.top && st.comb == COMB_ACTIVE_LEAF))) {
             auto it = push_maps.find(st.p);
             if (it != push_maps.end()) {
                 st.map_off = it->second;
@@ -595,15 +680,36 @@ static void plan_vp_extend(Plan &pl, int64_t n_local, int64_t n_global, int64_t 
 }
 
 sg2v_status make_plan(const Template &t, int64_t n, int64_t nnz, sg2v_precision prec, Layout layout,
-                      uint64_t budget, std::unique_ptr<Plan> &out, int64_t vp_n_global, int64_t vp_tile) {
+                      uint64_t budget, std::unique_ptr<Plan> &out, int64_t vp_n_global, int64_t vp_tile,
+                      int proj_mode) {
     std::unique_ptr<Plan> best, smallest;
     int r0 = 0, r1 = t.k - 1;
     if (t.root_hint >= 0) r0 = r1 = t.root_hint;
+    const bool try_proj = proj_mode > 0 && layout == LAYOUT_ANCHORED && vp_n_global == 0;
     for (int root = r0; root <= r1; ++root) {
         for (int policy = 0; policy < 3; ++policy) {
             Chain c = build_chain(t, root, policy);
             auto pl = std::make_unique<Plan>();
             plan_chain(t, c, root, n, nnz, prec, layout, *pl);
+            if (try_proj && !pl->proj_cands.empty()) {
+                // greedy: project the largest classes first while the plan fits the
+                // budget and the model says it is faster (proj_mode 2: every class that fits)
+                std::vector<std::string> cands = pl->proj_cands;
+                std::stable_sort(cands.begin(), cands.end(),
+                                 [](const std::string &a, const std::string &b) { return a.size() > b.size(); });
+                std::set<std::string> chosen;
+                for (const std::string &cl : cands) {
+                    std::set<std::string> trial = chosen;
+                    trial.insert(cl);
+                    Plan q;
+                    plan_chain(t, c, root, n, nnz, prec, layout, q, trial);
+                    const bool qfits = budget == 0 || (uint64_t)q.ws_bytes <= budget;
+                    if (qfits && (proj_mode == 2 || q.model_time < pl->model_time * (1 - 1e-6))) {
+                        chosen = trial;
+                        *pl = std::move(q);
+                    }
+                }
+            }
             const bool fits = budget == 0 || (uint64_t)pl->ws_bytes <= budget;
             if (!smallest || pl->ws_bytes < smallest->ws_bytes) {
                 smallest = std::make_unique<Plan>(*pl);
@@ -640,7 +746,9 @@ std::string Plan::describe() const {
           << ",\"comb\":\"" << (s.comb == COMB_ACTIVE_LEAF ? "active_leaf" : "general") << "\""
           << ",\"cs\":" << s.cs << ",\"ca\":" << s.ca << ",\"cp\":" << s.cp
           << ",\"cb\":" << s.cb << ",\"lds\":" << s.lds << ",\"ldp\":" << s.ldp << ",\"nterms\":" << s.nterms
-          << ",\"self\":" << (s.self_a ? "true" : "false") << ",\"gt\":" << s.gt << ",\"alg_bytes\":" << s.alg_bytes << ",\"ema_terms\":" << s.ema_terms << "}";
+          << ",\"self\":" << (s.self_a ? "true" : "false")
+          << ",\"proj_out\":" << (s.proj_out ? "true" : "false") << ",\"proj_p\":" << (s.proj_p ? "true" : "false")
+ << ",\"gt\":" << s.gt << ",\"alg_bytes\":" << s.alg_bytes << ",\"ema_terms\":" << s.ema_terms << "}";
     }
     o << "]}";
     return o.str();

@@ -6,6 +6,7 @@
 #include <cstdint>
 #include <map>
 #include <memory>
+#include <set>
 #include <string>
 #include <tuple>
 #include <vector>
@@ -69,6 +70,11 @@ struct Step {
     int64_t nterms = 0;                    // splits per output (GENERAL)
     int packed = 0;                        // anchored GENERAL: pairs packed ia | ip << 16, term-major
     bool self_a = false;                   // anchored: T_s = root + 2 copies of X, M_a(i,·) = B(i,·)
+    // exclusion-projected tables (anchored): a row holds, for every consumer colour
+    // y ≠ c(i), the segment of its sets avoiding y (C(k-2,·-1) entries, stride ldseg)
+    bool proj_out = false, proj_p = false;
+    int64_t ldseg_out = 0, ldseg_p = 0;
+    int64_t omap_off = -1;                 // projected output: write map (int32 offset)
     std::string canon_out, canon_a, canon_p;  // rooted classes of T_s, T_a, T_p (table sharing)
     int gt = 32;                           // threads per row group (step kernel)
     double alg_bytes = 0.0;                // algorithmic HBM bytes
@@ -106,6 +112,9 @@ struct Plan {
     double model_time = 0.0;
     double alg_bytes_total = 0.0;
     int64_t hist_bytes = 0;
+    bool allow_proj = true;       // planner may choose exclusion-projected tables
+    std::vector<std::string> proj_cands;  // classes that could be projected (planning)
+    std::set<std::string> proj;   // classes stored projected
     std::string describe() const;
 };
 
@@ -130,7 +139,8 @@ struct Template {
 sg2v_status validate_template(int k, const int32_t *edges, Template &t);
 double automorphisms(const Template &t);
 sg2v_status make_plan(const Template &t, int64_t n, int64_t nnz, sg2v_precision prec, Layout layout,
-                      uint64_t budget, std::unique_ptr<Plan> &out, int64_t vp_n_global = 0, int64_t vp_tile = 0);
+                      uint64_t budget, std::unique_ptr<Plan> &out, int64_t vp_n_global = 0, int64_t vp_tile = 0,
+                      int proj_mode = 1);  // exclusion-projected tables: 0 off, 1 model, 2 all that fit
 int64_t binom(int n, int r);
 
 // kernels.cu — launchers; all return cudaError_t as int (0 = success)

@@ -64,9 +64,10 @@ def lib():
     """dlopen libsg2v.so (raises if it was not built — no fallback)."""
     global _lib
     if _lib is None:
-        if not os.path.exists(LIB):
-            raise RuntimeError(f"{LIB} missing: run __graft_entry__.build() (no CPU fallback exists)")
-        L = ctypes.CDLL(LIB)
+        lib = os.environ.get("SG2V_LIB", LIB)  # A/B experiments against another build of the library
+        if not os.path.exists(lib):
+            raise RuntimeError(f"{lib} missing: run __graft_entry__.build() (no CPU fallback exists)")
+        L = ctypes.CDLL(lib)
         vp, i64, i32, u64 = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32, ctypes.c_uint64
         P = ctypes.POINTER
         L.sg2v_graph_load_csr.argtypes = [i64, vp, vp, i64, ctypes.c_uint32, P(vp)]
@@ -217,7 +218,7 @@ def template_build(k, edges, root_hint=-1) -> Template:
     return Template(h, int(k), list(edges))
 
 
-LAYOUTS = {"anchored": 0, "dense": 1}
+LAYOUTS = {"anchored": 0, "dense": 1, "anchored_plain": 2, "anchored_proj": 3}
 
 
 def _set_layout(layout, mem_budget_bytes=0):

@@ -94,14 +94,16 @@ def test_plan_invariants(name):
         assert a["layout"] == "anchored" and len(a["steps"]) <= k - 1
         for s in a["steps"]:
             assert s["s"] == s["a"] + s["p"]
-            assert s["cp"] == math.comb(k - 1, s["p"] - 1)
+            # exclusion-projected passive table: one segment of C(k-2,p-1) sets is gathered
+            assert s["cp"] == math.comb(k - 2 if s["proj_p"] else k - 1, s["p"] - 1)
             assert s["cb"] == math.comb(k - 1, s["p"])
             if not s["top"]:
                 assert s["cs"] == math.comb(k - 1, s["s"] - 1)
             if s["comb"] == "general":
                 assert s["nterms"] == (math.comb(k - 1, s["a"] - 1) if s["top"] else math.comb(s["s"] - 1, s["a"] - 1))
         if k >= 4:
-            assert a["tables_bytes"] < d["tables_bytes"]
+            plain = sg.plan_describe_n(1 << 20, 200 << 20, T, prec, "anchored_plain")
+            assert plain["tables_bytes"] < d["tables_bytes"]
 
 
 def test_root_hint_changes_plan_not_sizes():
@@ -150,3 +152,27 @@ def test_isomorphic_subtemplates_share_tables():
     # stars: every leaf arm is the same class; the first split (centre + 2 leaves) is a self step
     S = sg.template_build(9, star_template(9))
     assert len(sg.plan_describe_n(1000, 8000, S, "u64")["steps"]) == 7  # 3 = 1 + 2 leaves is a self step
+
+
+def test_exclusion_projected_tables_planned():
+    # u15-1 on RMAT-1M-like: with memory to spare the planner stores the 7-vertex arm
+    # read by the top self step as k-1 per-consumer-colour segments of C(13,6) sets
+    # (1716 instead of 3003 gathered per neighbour); layout "anchored_plain" never does
+    T = sg.template_build(15, path_template(15), root_hint=7)
+    d = sg.plan_describe_n(1 << 20, 208_236_700, T, "f32", mem_budget_bytes=170 << 30)
+    top = d["steps"][-1]
+    assert top["proj_p"] and top["cp"] == math.comb(13, 6) and top["ldp"] == 14 * 1716
+    prod = [s for s in d["steps"] if s["proj_out"]]
+    assert prod and all(s["lds"] == 14 * (-(-math.comb(13, s["s"] - 1) // 4) * 4) for s in prod)
+    assert d["workspace_bytes"] <= 170 << 30
+    plain = sg.plan_describe_n(1 << 20, 208_236_700, T, "f32", "anchored_plain", mem_budget_bytes=170 << 30)
+    assert not any(s["proj_out"] or s["proj_p"] for s in plain["steps"])
+    assert plain["model_seconds"] > d["model_seconds"]
+    assert plain["workspace_bytes"] < d["workspace_bytes"]
+    # a tight budget keeps the plain plan
+    tight = sg.plan_describe_n(1 << 20, 208_236_700, T, "f32", mem_budget_bytes=30 << 30)
+    assert tight["workspace_bytes"] <= 30 << 30
+    # every consumer of a projected class reads it as a projected passive table
+    for s in d["steps"]:
+        if s["proj_p"]:
+            assert s["src"] == "gather" and not (s["top"] and s["comb"] == "active_leaf")

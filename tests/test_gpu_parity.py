@@ -34,7 +34,9 @@ def _load(g):
     return sg.graph_load_csr(g.n, g.row_offsets, g.col_indices, validate=True)
 
 
-LAYOUTS = ("anchored", "dense")
+# anchored without / with every eligible exclusion-projected table (the default
+# "anchored" picks between the two per class), dense
+LAYOUTS = ("anchored_plain", "anchored_proj", "dense")
 
 
 def _rows(G, T, seed, j, prec, layout="anchored"):
@@ -138,6 +140,12 @@ def test_wide_rows_multiple_passes(oracle):
     # u15-1: c_p up to C(15,7)=6435 -> several 1024-vector passes per row (fp32) and
     # odd widths (ragged tails of the 16-B vectors); also u12-1
     g = erdos_renyi(1500, 9000, seed=4)
+    # "anchored_proj" plans use exclusion-projected tables (written by leaf-active
+    # copies; read by projected gathers)
+    G = _load(g)
+    for name in ("u15-1", "u12-1"):
+        d = sg.plan_describe(G, sg.template_build(_k(TEMPLATES[name]), TEMPLATES[name]), "u64", "anchored_proj")
+        assert any(s["proj_p"] for s in d["steps"]) and any(s["proj_out"] for s in d["steps"]), name
     _check_all(oracle, g, TEMPLATES["u15-1"], [(1, 0)], precs=("u64", "f64", "f32"))
     _check_all(oracle, g, TEMPLATES["u12-1"], [(2, 5)], roots=(-1, 0, 5))
 
