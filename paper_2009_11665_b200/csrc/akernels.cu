@@ -100,7 +100,9 @@ struct AStepArgs {
     const int32_t *pmap;  // push map [x][c(i)][cp] -> B column or -1
     int64_t ldseg_p;    // > 0: the passive table is exclusion-projected: k-1 segments of
                         //   ldseg_p elements per row, segment y' = sets avoiding colour y
-    int64_t ldseg_out;  // > 0: write the output table exclusion-projected (stride lds)
+    int64_t ldseg_out;  // > 0: write the exclusion-projected output table msx (stride ldsx)
+    char *msx;
+    int64_t ldsx;
     const int32_t *omap;  // its write map (leaf-active: inverse [y'][ldseg_out]; general:
                           //   forward [o][k-1] -> position in segment y', or -1)
     int64_t ocols;      // eMA outputs per row, padded to 16 B
@@ -180,8 +182,7 @@ __device__ __forceinline__ void gather_row(const AStepArgs &A, int64_t i, int ci
                         for (int q = 0; q < R; ++q) {
                             const int64_t v = v0 + q * GT + t;
                             const char *src = A.mp + (size_t)jj[u] * row_bytes + sbase + (v - t) * 16;
-                            xv[u][q] = need[q] ? (A.hint ? ldg16_pol(src, pol[u]) : ldg16(src))
-                                               : make_uint4(0, 0, 0, 0);
+                            xv[u][q] = ldg16_pred(src, need[q], pol[u]);
                         }
 #pragma unroll
                     for (int u = 0; u < U; ++u)
@@ -192,10 +193,12 @@ __device__ __forceinline__ void gather_row(const AStepArgs &A, int64_t i, int ci
                     constexpr int UT = U < 8 ? U : 8;
                     for (; e2 < e3; e2 += UT) {
                         int32_t jj[UT];
+                        uint64_t pol[UT];
 #pragma unroll
                         for (int u = 0; u < UT; ++u) {
                             const int32_t b1 = (e2 + u < e3) ? __ldg(A.bcol + e2 + u) : -1;
                             jj[u] = (b1 >= 0 && A.tagged) ? (b1 & kIdMask) : b1;
+                            pol[u] = (A.tagged && b1 >= 0 && (b1 >> kClassShift) < A.hot_log2) ? pol_last : pol_first;
                         }
                         uint4 xv[UT][R];
 #pragma unroll
@@ -203,8 +206,8 @@ __device__ __forceinline__ void gather_row(const AStepArgs &A, int64_t i, int ci
 #pragma unroll
                             for (int q = 0; q < R; ++q) {
                                 const int64_t v = v0 + q * GT + t;
-                                xv[u][q] = (jj[u] >= 0 && need[q]) ? ldg16(A.mp + (size_t)jj[u] * row_bytes + sbase + (v - t) * 16)
-                                                                   : make_uint4(0, 0, 0, 0);
+                                xv[u][q] = ldg16_pred(A.mp + (size_t)(jj[u] >= 0 ? jj[u] : 0) * row_bytes + sbase + (v - t) * 16,
+                                                      jj[u] >= 0 && need[q], pol[u]);
                             }
 #pragma unroll
                         for (int u = 0; u < UT; ++u)
@@ -240,8 +243,17 @@ __device__ __forceinline__ void gather_row(const AStepArgs &A, int64_t i, int ci
 // MODE: 0 = fused single-GPU step, 1 = vertex-partitioned column-tile gather into
 // bg rows, 2 = vertex-partitioned combine from bg (compile-time so the fused
 // kernel keeps its register allocation).
+// Register budget: the single-row gather variants keep 3 (U = 16) or 4 (U = 8) CTAs of
+// 256 threads per SM (<= 80 / 64 registers), the V-row eMA variants 2 (<= 128) —
+// ptxas otherwise spends registers on the epilogue paths / eMA unrolling and loses
+// CTAs of memory parallelism per SM.
+template <int U, int V, int MODE>
+struct AStepMinBlocks {
+    static constexpr int value = MODE != 0 ? 1 : V == 1 ? (U >= 16 ? 3 : 4) : 2;
+};
+
 template <typename T, typename RT, int GT, int R, int U, int V, int MODE>
-__global__ void __launch_bounds__(256) astep_kernel(AStepArgs A) {
+__global__ void __launch_bounds__(256, AStepMinBlocks<U, V, MODE>::value) astep_kernel(AStepArgs A) {
     constexpr int G = 256 / GT;
     constexpr int VN = Vec<T>::N;
     extern __shared__ __align__(16) unsigned char smem[];
@@ -250,7 +262,9 @@ __global__ void __launch_bounds__(256) astep_kernel(AStepArgs A) {
     T *sBase = reinterpret_cast<T *>(smem) + (size_t)g * V * A.smem_group;
     const int64_t per_slot = (int64_t)G * V;
     const int64_t nslots = (A.n + per_slot - 1) / per_slot;
-    const uint64_t pol_last = policy_evict_last(), pol_first = policy_evict_first();
+    // L2 policies of the gathers: hub rows evict_last, the rest evict_first (no hints:
+    // evict_normal for everything, e.g. the re-read staging tiles of the vertex mode)
+    const uint64_t pol_last = policy_evict_last(), pol_first = A.hint ? policy_evict_first() : policy_evict_normal();
 
     for (int64_t slot = blockIdx.x; slot < nslots; slot += gridDim.x) {
         int64_t iv[V];
@@ -326,11 +340,16 @@ __global__ void __launch_bounds__(256) astep_kernel(AStepArgs A) {
 #pragma unroll
             for (int v = 0; v < V; ++v)
                 if (actv[v]) {
-                    T *out = reinterpret_cast<T *>(A.ms) + (size_t)iv[v] * A.lds;
                     const T *sB = sBase + (size_t)v * A.smem_group;
-                    if (A.ldseg_out > 0) {
+                    if (A.ms) {  // plain table
+                        T *out = reinterpret_cast<T *>(A.ms) + (size_t)iv[v] * A.lds;
+                        for (int64_t q = t; q < A.lds / VN; q += GT)
+                            reinterpret_cast<uint4 *>(out)[q] = reinterpret_cast<const uint4 *>(sB)[q];
+                    }
+                    if (A.msx) {
                         // projected: segment y' position u <- B(i, omap[y'][u]) (16-B stores)
-                        for (int64_t q = t; q < A.lds / VN; q += GT) {
+                        T *out = reinterpret_cast<T *>(A.msx) + (size_t)iv[v] * A.ldsx;
+                        for (int64_t q = t; q < A.ldsx / VN; q += GT) {
                             uint4 w;
 #pragma unroll
                             for (int el = 0; el < VN; ++el) {
@@ -339,9 +358,6 @@ __global__ void __launch_bounds__(256) astep_kernel(AStepArgs A) {
                             }
                             reinterpret_cast<uint4 *>(out)[q] = w;
                         }
-                    } else {
-                        for (int64_t q = t; q < A.lds / VN; q += GT)
-                            reinterpret_cast<uint4 *>(out)[q] = reinterpret_cast<const uint4 *>(sB)[q];
                     }
                 }
         } else if (!A.top) {
@@ -417,15 +433,14 @@ __global__ void __launch_bounds__(256) astep_kernel(AStepArgs A) {
                             if (off < tpo) acc[v] += __shfl_xor_sync(0xffffffffu, acc[v], off);
                     }
                     if (actv[v] && l == 0 && o < lds) {
-                        T *orow = reinterpret_cast<T *>(A.ms) + (size_t)iv[v] * A.lds;
-                        if (A.ldseg_out > 0) {  // projected: every segment y' ∌ o
-                            if (o < cs)
-                                for (int y = 0; y < A.k - 1; ++y) {
-                                    const int32_t pos = __ldg(A.omap + (size_t)o * (A.k - 1) + y);
-                                    if (pos >= 0) orow[(size_t)y * A.ldseg_out + pos] = acc[v];
-                                }
-                        } else {
-                            orow[o] = acc[v];
+                        if (A.ms) reinterpret_cast<T *>(A.ms)[(size_t)iv[v] * A.lds + o] = acc[v];
+                        if (A.msx && o < cs) {  // projected: every segment y' ∌ o
+                            T *orow = reinterpret_cast<T *>(A.msx) + (size_t)iv[v] * A.ldsx;
+#pragma unroll 1
+                            for (int y = 0; y < A.k - 1; ++y) {
+                                const int32_t pos = __ldg(A.omap + (size_t)o * (A.k - 1) + y);
+                                if (pos >= 0) orow[(size_t)y * A.ldseg_out + pos] = acc[v];
+                            }
                         }
                     }
                 }
@@ -528,8 +543,9 @@ static int launch_astep_t(const AStepArgs &A, void *stream) {
 
 // Row-group configuration: narrow rows give every vector of the passive row its own
 // lane (R = 1) and keep U = 8 neighbours in flight; rows wider than 256 vectors use
-// the whole CTA, one vector per lane per pass with U = 16 neighbours in flight
-// (measured best of R/U in {1/16, 2/8, 4/4} on u15-1, RMAT-1M-like).
+// the whole CTA, one vector per lane per pass, also U = 8 (64 registers, 4 CTAs per
+// SM; on RMAT-1M-like graphs a colour bucket holds ~200/k neighbours, so most loads
+// are issued by the 8-wide tail batch anyway; U = 16 at 3 CTAs/SM measured 5 % slower).
 template <typename T, typename RT, int R, int U, int MODE = 0>
 static int launch_astep_gt(const AStepArgs &A, int gt, void *stream) {
     switch (gt) {
@@ -547,7 +563,8 @@ template <typename T, typename RT, int MODE = 0>
 static int launch_astep_cfg(const AStepArgs &A0, void *stream) {
     AStepArgs A = A0;
     constexpr int VN = Vec<T>::N;
-    static int tune = -1;  // SG2V_TUNE (experiments only): 1 narrow U=16; 2 wide R=2/U=8; 4 wide R=4/U=4; 5 no V-rows
+    static int tune = -1;  // SG2V_TUNE (experiments only): 1 narrow U=16; 2 wide R=2/U=8; 4 wide R=4/U=4; 5 no V-rows;
+                           // 16 wide U=16 (default U=8 under the 4-CTA register cap: measured faster, r1s18)
     if (tune < 0) {
         const char *e = getenv("SG2V_TUNE");
         tune = e ? atoi(e) : 0;
@@ -595,7 +612,8 @@ static int launch_astep_cfg(const AStepArgs &A0, void *stream) {
     if (nvec > 256) {
         if (tune == 2) return launch_astep_t<T, RT, 256, 2, 8>(A, stream);
         if (tune == 4) return launch_astep_t<T, RT, 256, 4, 4>(A, stream);
-        return launch_astep_t<T, RT, 256, 1, 16>(A, stream);
+        if (tune == 16) return launch_astep_t<T, RT, 256, 1, 16>(A, stream);
+        return launch_astep_t<T, RT, 256, 1, 8>(A, stream);
     }
     if (tune == 1) return launch_astep_gt<T, RT, 1, 16>(A, gt, stream);
     return launch_astep_gt<T, RT, 1, 8>(A, gt, stream);
@@ -646,11 +664,13 @@ int launch_astep_vp(const Graph &g, const Plan &pl, const Step &st, const uint8_
     A.pmap = st.map_off >= 0 ? pl.d_index + st.map_off : nullptr;
     A.ma = (st.comb == COMB_GENERAL && st.buf_a >= 0) ? tables + pl.bufs[st.buf_a].offset : nullptr;
     A.lda = st.lda;
-    A.ms = st.top ? nullptr : tables + pl.bufs[st.buf_out].offset;
+    A.ms = (st.top || st.buf_out < 0) ? nullptr : tables + pl.bufs[st.buf_out].offset;
     A.lds = st.lds;
     A.cs = st.cs;
     A.ldseg_p = st.proj_p ? st.ldseg_p : 0;
     A.ldseg_out = st.proj_out ? st.ldseg_out : 0;
+    A.msx = (!st.top && st.proj_out && st.buf_outx >= 0) ? tables + pl.bufs[st.buf_outx].offset : nullptr;
+    A.ldsx = st.ldsx;
     A.omap = st.omap_off >= 0 ? pl.d_index + st.omap_off : nullptr;
     A.ocols = st.top ? 1 : (st.cs + (16 / pl.elem) - 1) / (16 / pl.elem) * (16 / pl.elem);
     A.ldb = st.ldb;

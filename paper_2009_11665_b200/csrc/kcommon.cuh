@@ -58,9 +58,26 @@ __device__ __forceinline__ uint4 ldg16_pol(const void *p, uint64_t pol) {
                  : "l"(p), "l"(pol));
     return r;
 }
+// predicated 128-bit load with an L2 policy: zero when !pred.  The predicate is
+// applied to the load instruction itself (no branch), so a batch of these stays
+// in flight together whatever control flow the compiler would otherwise choose.
+__device__ __forceinline__ uint4 ldg16_pred(const void *p, bool pred, uint64_t pol) {
+    uint4 r = make_uint4(0, 0, 0, 0);
+    asm volatile(
+        "{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %4, 0;\n\t"
+        "@q ld.global.nc.L2::cache_hint.v4.u32 {%0,%1,%2,%3}, [%5], %6;\n\t}"
+        : "+r"(r.x), "+r"(r.y), "+r"(r.z), "+r"(r.w)
+        : "r"((int)pred), "l"(p), "l"(pol));
+    return r;
+}
 __device__ __forceinline__ uint64_t policy_evict_last() {
     uint64_t p;
     asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ uint64_t policy_evict_normal() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(p));
     return p;
 }
 __device__ __forceinline__ uint64_t policy_evict_first() {

@@ -257,7 +257,7 @@ static bool plan_chain(const Template &t, const Chain &c, int root, int64_t n, i
     for (size_t i = 0; i < pl.nodes.size(); ++i) {
         const Node &nd = pl.nodes[i];
         if (nd.active >= 0 && (int)i != c.top && proj.count(canon[i]))
-            out_bytes[i] = n * (int64_t)(k - 1) * round_up(binom(k - 2, nd.size - 1), vn) * pl.elem;
+            out_bytes[i] += n * (int64_t)(k - 1) * round_up(binom(k - 2, nd.size - 1), vn) * pl.elem;
     }
     std::vector<int> sched;
     std::function<int64_t(int, std::vector<int> &)> order = [&](int v, std::vector<int> &seq) -> int64_t {
@@ -324,34 +324,38 @@ static bool plan_chain(const Template &t, const Chain &c, int root, int64_t n, i
         };
         visit(c.top);
     }
-    // Exclusion-projected tables: a class read only as the PASSIVE side of row-streaming
-    // gathers may be stored as k-1 segments per row, one per consumer colour y ≠ c(i),
-    // holding the sets that avoid y (C(k-2,s-1) entries): a consumer of colour c(i)
-    // streams exactly the sets it can use instead of the whole C(k-1,s-1) row (where
-    // a fraction (s-1)/(k-1) contain c(i) and are discarded), for k-s times the table
-    // memory.  The planner picks the classes (make_plan).
+    // Exclusion-projected tables: a class read as the PASSIVE side of row-streaming
+    // gathers may (also) be stored as k-1 segments per row, one per consumer colour
+    // y ≠ c(i), holding the sets that avoid y (C(k-2,s-1) entries): a consumer of
+    // colour c(i) streams exactly the sets it can use instead of the whole C(k-1,s-1)
+    // row (where a fraction (s-1)/(k-1) contain c(i) and are discarded), for k-s times
+    // the table memory.  A class that is also read as an active child M_a (or by a
+    // top step with a leaf active child, one column per edge) keeps its plain table
+    // too ("dual").  The planner picks the classes (make_plan).
+    // gather_reader(v): step v streams its passive child's rows
+    auto gather_reader = [&](int v) {
+        const Node &nd = pl.nodes[v];
+        return anch && pl.nodes[nd.passive].size > 1 && !(v == c.top && pl.nodes[nd.active].size == 1);
+    };
     {
-        std::map<std::string, bool> ok;
-        for (int v : sched) {
-            const Node &nd = pl.nodes[v];
-            const bool top = (v == c.top);
-            const int a = pl.nodes[nd.active].size, p = pl.nodes[nd.passive].size;
-            if (!self_step(v) && a > 1) ok[canon[nd.active]] = false;  // read as M_a
-            if (p > 1) {
-                const bool top_leaf = top && a == 1;                   // one column per edge
-                auto it = ok.find(canon[nd.passive]);
-                ok[canon[nd.passive]] = (it == ok.end() || it->second) && !top_leaf && anch;
+        std::set<std::string> seen;
+        for (int v : sched)
+            if (gather_reader(v) && !seen.count(canon[pl.nodes[v].passive])) {
+                seen.insert(canon[pl.nodes[v].passive]);
+                pl.proj_cands.push_back(canon[pl.nodes[v].passive]);
             }
-        }
-        for (auto &kv : ok)
-            if (kv.second) pl.proj_cands.push_back(kv.first);
     }
-    auto key = [&](int v) { return proj.count(canon[v]) ? canon[v] + "|x" : canon[v]; };
-    // uses of each class by the scheduled steps (a table is freed after its last use)
+    // table key read by step v for its passive child: the projected copy when the class
+    // is projected and v streams it, else the plain table
+    auto pkey = [&](int v) {
+        const std::string &cp = canon[pl.nodes[v].passive];
+        return proj.count(cp) && gather_reader(v) ? cp + "|x" : cp;
+    };
+    // uses of each table by the scheduled steps (a table is freed after its last use)
     std::map<std::string, int> uses;
     for (int v : sched) {
-        if (!self_step(v)) uses[key(pl.nodes[v].active)]++;
-        uses[key(pl.nodes[v].passive)]++;
+        if (!self_step(v)) uses[canon[pl.nodes[v].active]]++;
+        uses[pkey(v)]++;
     }
 
     // --- first-fit arena over the schedule ---
@@ -392,11 +396,12 @@ static bool plan_chain(const Template &t, const Chain &c, int root, int64_t n, i
         st.cp = table_width(L, k, st.p);
         st.cb = anch ? binom(k - 1, st.p) : st.cp;
         st.proj_out = !st.top && proj.count(canon[v]);
-        st.proj_p = st.src == SRC_GATHER && proj.count(canon[nd.passive]);
+        st.plain_out = !st.top && uses.count(canon[v]) && uses[canon[v]] > 0;  // someone reads the plain table
+        st.proj_p = st.src == SRC_GATHER && proj.count(canon[nd.passive]) && gather_reader(v);
         st.lds = st.top ? 1 : round_up(st.cs, vn);
         if (st.proj_out) {
             st.ldseg_out = round_up(binom(k - 2, st.s - 1), vn);
-            st.lds = (int64_t)(k - 1) * st.ldseg_out;
+            st.ldsx = (int64_t)(k - 1) * st.ldseg_out;
         }
         st.lda = round_up(st.ca, vn);
         st.ldp = (st.src == SRC_HIST) ? round_up(k, vn) : round_up(st.cp, vn);
@@ -407,13 +412,13 @@ static bool plan_chain(const Template &t, const Chain &c, int root, int64_t n, i
         }
         st.ldb = anch ? round_up(st.cb, vn) : st.ldp;
         st.self_a = self_step(v);
-        st.canon_out = key(v);
-        st.canon_a = key(nd.active);
-        st.canon_p = key(nd.passive);
+        st.canon_out = canon[v];
+        st.canon_a = canon[nd.active];
+        st.canon_p = pkey(v);
         st.buf_a = (!st.self_a && class_buf.count(st.canon_a)) ? class_buf[st.canon_a] : -1;
         st.buf_p = class_buf.count(st.canon_p) ? class_buf[st.canon_p] : -1;
         if (st.src == SRC_HIST && !anch) pl.need_hist = true;
-        if (!st.top) {
+        if (st.plain_out) {
             Buffer b;
             b.bytes = n * st.lds * pl.elem;
             b.offset = alloc(b.bytes);
@@ -421,6 +426,14 @@ static bool plan_chain(const Template &t, const Chain &c, int root, int64_t n, i
             st.buf_out = (int)pl.bufs.size() - 1;
             node_buf[v] = st.buf_out;
             class_buf[st.canon_out] = st.buf_out;
+        }
+        if (st.proj_out) {
+            Buffer b;
+            b.bytes = n * st.ldsx * pl.elem;
+            b.offset = alloc(b.bytes);
+            pl.bufs.push_back(b);
+            st.buf_outx = (int)pl.bufs.size() - 1;
+            class_buf[st.canon_out + "|x"] = st.buf_outx;
         }
         if (!st.self_a && --uses[st.canon_a] == 0) release(st.buf_a);
         if (--uses[st.canon_p] == 0) release(st.buf_p);
@@ -444,7 +457,8 @@ static bool plan_chain(const Template &t, const Chain &c, int root, int64_t n, i
                             ? nnz * 4.0 + nnz * live_frac * (double)round_up(st.cp * pl.elem, 32) + n * 12.0
                             : hsrc;
             double ma = (st.comb == COMB_GENERAL && !st.self_a) ? n * (double)st.ca * E : n * 1.0;
-            double w = st.top ? n * 8.0 : st.proj_out ? n * (double)st.lds * E : n * (double)st.cs * E;
+            double w = st.top ? n * 8.0
+                              : (st.plain_out ? n * (double)st.cs * E : 0.0) + (st.proj_out ? n * (double)st.ldsx * E : 0.0);
             bytes = gather + ma + w;
             mbytes = mg + ma + w;
             if (anch && st.src == SRC_GATHER)  // per-row push of k-1 colour partial sums through smem
@@ -748,6 +762,7 @@ std::string Plan::describe() const {
           << ",\"cb\":" << s.cb << ",\"lds\":" << s.lds << ",\"ldp\":" << s.ldp << ",\"nterms\":" << s.nterms
           << ",\"self\":" << (s.self_a ? "true" : "false")
           << ",\"proj_out\":" << (s.proj_out ? "true" : "false") << ",\"proj_p\":" << (s.proj_p ? "true" : "false")
+          << ",\"plain_out\":" << (s.plain_out ? "true" : "false") << ",\"ldsx\":" << s.ldsx
  << ",\"gt\":" << s.gt << ",\"alg_bytes\":" << s.alg_bytes << ",\"ema_terms\":" << s.ema_terms << "}";
     }
     o << "]}";

@@ -73,7 +73,9 @@ struct Step {
     // exclusion-projected tables (anchored): a row holds, for every consumer colour
     // y ≠ c(i), the segment of its sets avoiding y (C(k-2,·-1) entries, stride ldseg)
     bool proj_out = false, proj_p = false;
-    int64_t ldseg_out = 0, ldseg_p = 0;
+    bool plain_out = false;                // the plain table is written (someone reads it)
+    int64_t ldseg_out = 0, ldseg_p = 0, ldsx = 0;   // ldsx: projected row stride (k-1)·ldseg_out
+    int buf_outx = -1;                     // projected output buffer
     int64_t omap_off = -1;                 // projected output: write map (int32 offset)
     std::string canon_out, canon_a, canon_p;  // rooted classes of T_s, T_a, T_p (table sharing)
     int gt = 32;                           // threads per row group (step kernel)

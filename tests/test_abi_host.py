@@ -163,7 +163,7 @@ def test_exclusion_projected_tables_planned():
     top = d["steps"][-1]
     assert top["proj_p"] and top["cp"] == math.comb(13, 6) and top["ldp"] == 14 * 1716
     prod = [s for s in d["steps"] if s["proj_out"]]
-    assert prod and all(s["lds"] == 14 * (-(-math.comb(13, s["s"] - 1) // 4) * 4) for s in prod)
+    assert prod and all(s["ldsx"] == 14 * (-(-math.comb(13, s["s"] - 1) // 4) * 4) for s in prod)
     assert d["workspace_bytes"] <= 170 << 30
     plain = sg.plan_describe_n(1 << 20, 208_236_700, T, "f32", "anchored_plain", mem_budget_bytes=170 << 30)
     assert not any(s["proj_out"] or s["proj_p"] for s in plain["steps"])
@@ -176,3 +176,14 @@ def test_exclusion_projected_tables_planned():
     for s in d["steps"]:
         if s["proj_p"]:
             assert s["src"] == "gather" and not (s["top"] and s["comb"] == "active_leaf")
+
+
+def test_dual_tables_for_classes_read_as_active_and_passive():
+    # u12-1 rooted at vertex 5: the top 12 = 6 + 6 reads the 6-vertex end-rooted path
+    # both as M_a (plain table) and as the gathered passive child (projected copy)
+    T = sg.template_build(12, path_template(12), root_hint=5)
+    d = sg.plan_describe_n(1 << 20, 208_236_700, T, "f32", mem_budget_bytes=170 << 30)
+    top = d["steps"][-1]
+    assert (top["s"], top["a"], top["p"]) == (12, 6, 6) and top["proj_p"] and top["cp"] == math.comb(10, 5)
+    prod = [s for s in d["steps"] if s["s"] == 6 and not s["top"]][0]
+    assert prod["proj_out"] and prod["plain_out"]
