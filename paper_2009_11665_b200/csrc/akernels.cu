@@ -262,6 +262,8 @@ __global__ void __launch_bounds__(256, AStepMinBlocks<U, V, MODE>::value) astep_
     T *sBase = reinterpret_cast<T *>(smem) + (size_t)g * V * A.smem_group;
     const int64_t per_slot = (int64_t)G * V;
     const int64_t nslots = (A.n + per_slot - 1) / per_slot;
+    // Count-table rows are written with streaming stores (__stcs: read by a later
+    // launch only, so they should not displace the hub rows kept in L2).
     // L2 policies of the gathers: hub rows evict_last, the rest evict_first (no hints:
     // evict_normal for everything, e.g. the re-read staging tiles of the vertex mode)
     const uint64_t pol_last = policy_evict_last(), pol_first = A.hint ? policy_evict_first() : policy_evict_normal();
@@ -344,7 +346,7 @@ __global__ void __launch_bounds__(256, AStepMinBlocks<U, V, MODE>::value) astep_
                     if (A.ms) {  // plain table
                         T *out = reinterpret_cast<T *>(A.ms) + (size_t)iv[v] * A.lds;
                         for (int64_t q = t; q < A.lds / VN; q += GT)
-                            reinterpret_cast<uint4 *>(out)[q] = reinterpret_cast<const uint4 *>(sB)[q];
+                            __stcs(reinterpret_cast<uint4 *>(out) + q, reinterpret_cast<const uint4 *>(sB)[q]);
                     }
                     if (A.msx) {
                         // projected: segment y' position u <- B(i, omap[y'][u]) (16-B stores)
@@ -356,7 +358,7 @@ __global__ void __launch_bounds__(256, AStepMinBlocks<U, V, MODE>::value) astep_
                                 const int32_t c = __ldg(A.omap + q * VN + el);
                                 vset<T>(w, el, c >= 0 ? sB[c] : (T)0);
                             }
-                            reinterpret_cast<uint4 *>(out)[q] = w;
+                            __stcs(reinterpret_cast<uint4 *>(out) + q, w);
                         }
                     }
                 }
@@ -433,13 +435,13 @@ __global__ void __launch_bounds__(256, AStepMinBlocks<U, V, MODE>::value) astep_
                             if (off < tpo) acc[v] += __shfl_xor_sync(0xffffffffu, acc[v], off);
                     }
                     if (actv[v] && l == 0 && o < lds) {
-                        if (A.ms) reinterpret_cast<T *>(A.ms)[(size_t)iv[v] * A.lds + o] = acc[v];
+                        if (A.ms) __stcs(reinterpret_cast<T *>(A.ms) + (size_t)iv[v] * A.lds + o, acc[v]);
                         if (A.msx && o < cs) {  // projected: every segment y' ∌ o
                             T *orow = reinterpret_cast<T *>(A.msx) + (size_t)iv[v] * A.ldsx;
 #pragma unroll 1
                             for (int y = 0; y < A.k - 1; ++y) {
                                 const int32_t pos = __ldg(A.omap + (size_t)o * (A.k - 1) + y);
-                                if (pos >= 0) orow[(size_t)y * A.ldseg_out + pos] = acc[v];
+                                if (pos >= 0) __stcs(orow + (size_t)y * A.ldseg_out + pos, acc[v]);
                             }
                         }
                     }
@@ -612,7 +614,10 @@ static int launch_astep_cfg(const AStepArgs &A0, void *stream) {
     if (nvec > 256) {
         if (tune == 2) return launch_astep_t<T, RT, 256, 2, 8>(A, stream);
         if (tune == 4) return launch_astep_t<T, RT, 256, 4, 4>(A, stream);
-        if (tune == 16) return launch_astep_t<T, RT, 256, 1, 16>(A, stream);
+        // very wide top steps (>= 4 passes, e.g. u16/u17 paths: 6435 / 11440 columns) keep
+        // 16 neighbours in flight (r1s20: u16-1 top 1201 -> 987 ms, u17-1 2069 -> 1718 ms);
+        // everything else U = 8 (u15-1: 0.799 -> 0.762 s)
+        if (tune == 16 || (A.top && nvec > 1024 && tune != 8)) return launch_astep_t<T, RT, 256, 1, 16>(A, stream);
         return launch_astep_t<T, RT, 256, 1, 8>(A, stream);
     }
     if (tune == 1) return launch_astep_gt<T, RT, 1, 16>(A, gt, stream);
