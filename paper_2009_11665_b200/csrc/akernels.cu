@@ -122,6 +122,7 @@ struct AStepArgs {
     int packed;         // split pairs packed as ia | ip << 16 (both < 2^16)
     int stage_a;        // M_a row staged in shared memory (else read through L1)
     int tpo;            // lanes per output in the eMA (power of 2, <= 32)
+    double terms_per_byte;  // eMA split terms per algorithmic byte of the step (launch config)
     int64_t aoff;       // offset of the M_a row in a group's shared memory: ldb, or 0 when
                         // M_a(i,·) IS B(i,·) (self step: T_s = root + two copies of X)
     // vertex-partitioned mode: B rows live in global memory
@@ -247,9 +248,12 @@ __device__ __forceinline__ void gather_row(const AStepArgs &A, int64_t i, int ci
 // 256 threads per SM (<= 80 / 64 registers), the V-row eMA variants 2 (<= 128) —
 // ptxas otherwise spends registers on the epilogue paths / eMA unrolling and loses
 // CTAs of memory parallelism per SM.
+#ifndef XP_MINB8
+#define XP_MINB8 4  // CTAs per SM of the U = 8 single-row variants (experiments: -DXP_MINB8=5)
+#endif
 template <int U, int V, int MODE>
 struct AStepMinBlocks {
-    static constexpr int value = MODE != 0 ? 1 : V == 1 ? (U >= 16 ? 3 : 4) : 2;
+    static constexpr int value = MODE != 0 ? 1 : V == 1 ? (U >= 16 ? 3 : XP_MINB8) : 2;
 };
 
 template <typename T, typename RT, int GT, int R, int U, int V, int MODE>
@@ -584,7 +588,13 @@ static int launch_astep_cfg(const AStepArgs &A0, void *stream) {
     if (A.comb == COMB_GENERAL && !A.top && gt >= 32)
         while (A.tpo < 32 && A.cs * A.tpo * 2 <= gt) A.tpo *= 2;
     // eMA-heavy GENERAL steps: V = 4 rows share every split-table load
+    static double vtpb = -1;  // SG2V_VTPB (experiments): the terms-per-byte threshold
+    if (vtpb < 0) { const char *e = getenv("SG2V_VTPB"); vtpb = e ? atof(e) : 0.05; }
+    // (only where the eMA is a real share of the step: >= 0.05 split terms per gathered
+    // byte; gather-dominated GENERAL steps such as u14-2's 13 = 5 + 8 (0.011) run one row
+    // per group so the gathers of different rows overlap)
     const bool multi = A.comb == COMB_GENERAL && !A.top && A.nterms >= 8 && gt >= 32 && tune != 5 &&
+                       (A.terms_per_byte >= vtpb || tune == 9) &&
                        (size_t)(256 / gt) * 4 * A.smem_group * sizeof(T) <= 200 * 1024;
     if constexpr (MODE != 0) {
         if constexpr (MODE == 2) {
@@ -676,6 +686,7 @@ int launch_astep_vp(const Graph &g, const Plan &pl, const Step &st, const uint8_
     A.ldseg_out = st.proj_out ? st.ldseg_out : 0;
     A.msx = (!st.top && st.proj_out && st.buf_outx >= 0) ? tables + pl.bufs[st.buf_outx].offset : nullptr;
     A.ldsx = st.ldsx;
+    A.terms_per_byte = st.alg_bytes > 0 ? st.ema_terms / st.alg_bytes : 1.0;
     A.omap = st.omap_off >= 0 ? pl.d_index + st.omap_off : nullptr;
     A.ocols = st.top ? 1 : (st.cs + (16 / pl.elem) - 1) / (16 / pl.elem) * (16 / pl.elem);
     A.ldb = st.ldb;
