@@ -19,6 +19,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdlib>
+#include <type_traits>
 
 #include "kcommon.cuh"
 #include "sg2v_internal.h"
@@ -132,6 +133,24 @@ struct AStepArgs {
     int bsrc_global;    // stage 1 = copy the completed B row from bg
     char *bg;           // [n_local][ldb] B rows (tile_mode / bsrc_global)
 };
+
+// F32 overflow flag: set by any anchored step that stores a non-finite table entry
+// (reset / read around every sg2v_count call; EOVERFLOW contract of sg2v.h).  Checked
+// at the stores, so the report does not depend on how inf / NaN propagate later.
+__device__ int g_ovf_flag;
+
+template <typename T>
+__device__ __forceinline__ bool nonfinite(T x) {
+    if constexpr (std::is_same<T, float>::value) return !isfinite(x);
+    else return false;
+}
+template <typename T>
+__device__ __forceinline__ bool nonfinite4(const uint4 &w) {
+    if constexpr (std::is_same<T, float>::value)
+        return !isfinite(__uint_as_float(w.x)) || !isfinite(__uint_as_float(w.y)) ||
+               !isfinite(__uint_as_float(w.z)) || !isfinite(__uint_as_float(w.w));
+    else return false;
+}
 
 // ---- stage 1 for one row: B(i,·) over T ⊂ [k]∖{c(i)} into sB (group-uniform) ----
 // STRIDE: element stride of B in sB (V when V rows are interleaved in shared memory)
@@ -272,6 +291,7 @@ __global__ void __launch_bounds__(256, AStepMinBlocks<U, V, MODE>::value) astep_
     // evict_normal for everything, e.g. the re-read staging tiles of the vertex mode)
     const uint64_t pol_last = policy_evict_last(), pol_first = A.hint ? policy_evict_first() : policy_evict_normal();
 
+    bool bad = false;  // a stored F32 entry is not finite
     for (int64_t slot = blockIdx.x; slot < nslots; slot += gridDim.x) {
         int64_t iv[V];
         bool actv[V];
@@ -349,8 +369,11 @@ __global__ void __launch_bounds__(256, AStepMinBlocks<U, V, MODE>::value) astep_
                     const T *sB = sBase + (size_t)v * A.smem_group;
                     if (A.ms) {  // plain table
                         T *out = reinterpret_cast<T *>(A.ms) + (size_t)iv[v] * A.lds;
-                        for (int64_t q = t; q < A.lds / VN; q += GT)
-                            __stcs(reinterpret_cast<uint4 *>(out) + q, reinterpret_cast<const uint4 *>(sB)[q]);
+                        for (int64_t q = t; q < A.lds / VN; q += GT) {
+                            const uint4 w = reinterpret_cast<const uint4 *>(sB)[q];
+                            bad |= nonfinite4<T>(w);
+                            __stcs(reinterpret_cast<uint4 *>(out) + q, w);
+                        }
                     }
                     if (A.msx) {
                         // projected: segment y' position u <- B(i, omap[y'][u]) (16-B stores)
@@ -362,6 +385,7 @@ __global__ void __launch_bounds__(256, AStepMinBlocks<U, V, MODE>::value) astep_
                                 const int32_t c = __ldg(A.omap + q * VN + el);
                                 vset<T>(w, el, c >= 0 ? sB[c] : (T)0);
                             }
+                            bad |= nonfinite4<T>(w);
                             __stcs(reinterpret_cast<uint4 *>(out) + q, w);
                         }
                     }
@@ -439,6 +463,7 @@ __global__ void __launch_bounds__(256, AStepMinBlocks<U, V, MODE>::value) astep_
                             if (off < tpo) acc[v] += __shfl_xor_sync(0xffffffffu, acc[v], off);
                     }
                     if (actv[v] && l == 0 && o < lds) {
+                        bad |= nonfinite<T>(acc[v]);
                         if (A.ms) __stcs(reinterpret_cast<T *>(A.ms) + (size_t)iv[v] * A.lds + o, acc[v]);
                         if (A.msx && o < cs) {  // projected: every segment y' ∌ o
                             T *orow = reinterpret_cast<T *>(A.msx) + (size_t)iv[v] * A.ldsx;
@@ -476,6 +501,7 @@ __global__ void __launch_bounds__(256, AStepMinBlocks<U, V, MODE>::value) astep_
         }
         group_sync<GT>(g);
     }
+    if (bad) atomicOr(&g_ovf_flag, 1);
 }
 
 // ---------------------------------------------------------------------------
@@ -512,6 +538,22 @@ __global__ void __launch_bounds__(256) atop_leaf_kernel(int64_t n, int k, int kp
 // ---------------------------------------------------------------------------
 // launchers
 // ---------------------------------------------------------------------------
+int ovf_reset(void *stream) {
+    void *p = nullptr;
+    cudaError_t e = cudaGetSymbolAddress(&p, g_ovf_flag);
+    if (e != cudaSuccess) return (int)e;
+    return (int)cudaMemsetAsync(p, 0, sizeof(int), (cudaStream_t)stream);
+}
+
+int ovf_read(int *flag, void *stream) {
+    void *p = nullptr;
+    cudaError_t e = cudaGetSymbolAddress(&p, g_ovf_flag);
+    if (e != cudaSuccess) return (int)e;
+    e = cudaMemcpyAsync(flag, p, sizeof(int), cudaMemcpyDeviceToHost, (cudaStream_t)stream);
+    if (e != cudaSuccess) return (int)e;
+    return (int)cudaStreamSynchronize((cudaStream_t)stream);
+}
+
 int launch_bucket(const Graph &g, const Plan &pl, const uint8_t *colors, int32_t *hcnt, int32_t *bcol,
                   void *stream) {
     if (g.n <= 0) return 0;

@@ -571,6 +571,8 @@ static sg2v_status count_vp(const sg2v_graph *g, const sg2v_template *t, int32_t
     cudaStream_t s = (cudaStream_t)o.stream;
     std::vector<double> resf(n_iter, 0.0);
     std::vector<uint64_t> resu(n_iter, 0);
+    int ovf = 0;
+    if (!u64mode && k > 1) SG2V_CK((cudaError_t)ovf_reset(s));
     if (k == 1) {
         for (int64_t q = 0; q < n_iter; ++q) { resf[q] = (double)n_global; resu[q] = (uint64_t)n_global; }
     } else {
@@ -681,8 +683,9 @@ static sg2v_status count_vp(const sg2v_graph *g, const sg2v_template *t, int32_t
             resu[q] = su;
             resf[q] = sf;
         }
+        if (!u64mode) SG2V_CK((cudaError_t)ovf_read(&ovf, s));
     }
-    bool finite = true;
+    bool finite = ovf == 0;  // a stored F32 table entry overflowed on this rank
     double sum = 0.0;
     for (int64_t q = 0; q < n_iter; ++q) {
         if (colorful_out) colorful_out[q] = u64mode ? (double)resu[q] : resf[q];
@@ -730,6 +733,7 @@ static sg2v_status count_core(const sg2v_graph *g, const sg2v_template *const *t
     const bool u64mode = o.precision == SG2V_U64;
     std::vector<double> resf((size_t)m * n_iter, 0.0);
     std::vector<uint64_t> resu((size_t)m * n_iter, 0);
+    int ovf = 0;
     cudaStream_t s = (cudaStream_t)o.stream;
 
     if (k == 1 || g->n == 0) {
@@ -787,6 +791,7 @@ static sg2v_status count_core(const sg2v_graph *g, const sg2v_template *const *t
         for (Plan *p : pls) need_hist = need_hist || p->need_hist;
         std::vector<uint64_t> host_ring((size_t)kResultsRing * m);
         int64_t base = 0;
+        if (!u64mode) SG2V_CK((cudaError_t)ovf_reset(s));
         for (int64_t q = 0; q < n_iter; ++q) {
             const int64_t j = o.iter_offset + q * o.iter_stride;
             int rc = launch_colorize(seed, j, g->n, k, colors, s);
@@ -825,8 +830,9 @@ static sg2v_status count_core(const sg2v_graph *g, const sg2v_template *const *t
             SG2V_CK(cudaMemcpyAsync(o.row_values, rowval, g->n * 8, cudaMemcpyDeviceToDevice, s));
             SG2V_CK(cudaStreamSynchronize(s));
         }
+        if (!u64mode && anch) SG2V_CK((cudaError_t)ovf_read(&ovf, s));
     }
-    bool finite = true;
+    bool finite = ovf == 0;  // a stored F32 table entry overflowed (set by the step kernels)
     for (int32_t tq = 0; tq < m; ++tq) {
         double sum = 0.0;
         for (int64_t q = 0; q < n_iter; ++q) {

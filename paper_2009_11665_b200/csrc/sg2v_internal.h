@@ -155,6 +155,8 @@ int launch_astep(const Graph &g, const Plan &pl, const Step &st, const uint8_t *
                  const int32_t *bcol, char *tables, void *rowval, void *stream);
 int launch_astep_vp(const Graph &g, const Plan &pl, const Step &st, const uint8_t *colors, const int32_t *hcnt,
                     const int32_t *bcol, char *tables, void *rowval, void *stream, const VpArgs *vp);
+int ovf_reset(void *stream);             // F32 overflow flag of the anchored steps
+int ovf_read(int *flag, void *stream);
 int launch_pack_tile(int64_t n, const char *src, int64_t ld_bytes, int64_t u0_bytes, int64_t w_bytes, char *dst,
                      int64_t dst_ld_bytes, void *stream);
 int launch_bg_rowval(const Plan &pl, int64_t n, const char *bg, int64_t ldb, void *rowval, void *stream);

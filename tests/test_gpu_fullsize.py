@@ -98,3 +98,28 @@ def test_u17_invariants():
     a = int(_count(G, sg.template_build(17, e), "u64"))
     b = int(_count(G, sg.template_build(17, e, root_hint=5), "u64"))
     assert a == b
+
+
+def test_f32_overflow_is_reported():
+    # u15-2 on RMAT-1M-like: hub rows push F32 table entries past 3.4e38 (the F64 count is
+    # ~1.6e47), so F32 must report EOVERFLOW — whichever kernel configuration ran (the
+    # V-row eMA path once returned a finite 0.0 here; the overflow flag is now set at the
+    # table stores).  U64 residues and F64 agree with the plain anchored layout.
+    g, G = _graph("rmat1m")
+    e = TEMPLATES["u15-2"]
+    T = sg.template_build(15, e)
+    def f32_status():
+        ws = sg.Workspace(sg.workspace_bytes(G, T, "f32"))
+        try:
+            sg.count(G, T, n_iter=1, seed=1, precision="f32", workspace=ws)
+            return 0
+        except sg.Sg2vError as ex:  # keep no traceback (it would pin the workspace)
+            return ex.code
+        finally:
+            del ws
+
+    assert f32_status() == 6  # EOVERFLOW
+    torch.cuda.empty_cache()
+    assert int(_count(G, T, "u64")) == int(_count(G, T, "u64", "anchored_plain"))
+    f64 = _count(G, T, "f64")
+    assert math.isfinite(f64) and f64 > 3.4e38
