@@ -272,7 +272,7 @@ __device__ __forceinline__ void gather_row(const AStepArgs &A, int64_t i, int ci
 #endif
 template <int U, int V, int MODE>
 struct AStepMinBlocks {
-    static constexpr int value = MODE != 0 ? 1 : V == 1 ? (U >= 16 ? 3 : XP_MINB8) : 2;
+    static constexpr int value = V == 1 ? (U >= 16 ? 3 : XP_MINB8) : 2;
 };
 
 template <typename T, typename RT, int GT, int R, int U, int V, int MODE>
