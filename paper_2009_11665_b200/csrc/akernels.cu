@@ -267,12 +267,15 @@ __device__ __forceinline__ void gather_row(const AStepArgs &A, int64_t i, int ci
 // 256 threads per SM (<= 80 / 64 registers), the V-row eMA variants 2 (<= 128) —
 // ptxas otherwise spends registers on the epilogue paths / eMA unrolling and loses
 // CTAs of memory parallelism per SM.
+#ifndef XP_MINB16
+#define XP_MINB16 3  // ... of the U = 16 variants
+#endif
 #ifndef XP_MINB8
 #define XP_MINB8 4  // CTAs per SM of the U = 8 single-row variants (experiments: -DXP_MINB8=5)
 #endif
 template <int U, int V, int MODE>
 struct AStepMinBlocks {
-    static constexpr int value = V == 1 ? (U >= 16 ? 3 : XP_MINB8) : 2;
+    static constexpr int value = V == 1 ? (U >= 16 ? XP_MINB16 : XP_MINB8) : 2;
 };
 
 template <typename T, typename RT, int GT, int R, int U, int V, int MODE>
