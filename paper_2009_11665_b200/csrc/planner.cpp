@@ -461,6 +461,11 @@ static bool plan_chain(const Template &t, const Chain &c, int root, int64_t n, i
                               : (st.plain_out ? n * (double)st.cs * E : 0.0) + (st.proj_out ? n * (double)st.ldsx * E : 0.0);
             bytes = gather + ma + w;
             mbytes = mg + ma + w;
+            // GENERAL projected outputs are scattered 4/8-B stores (one per output and
+            // segment): model a 32-B sector each (measured: u13-2's 8 = 7 + 1 projected ran
+            // slower than the plain plan the model had ranked below it)
+            if (st.proj_out && st.comb == COMB_GENERAL)
+                mbytes += n * (double)st.cs * (double)(k - st.s) * (32.0 - E);
             if (anch && st.src == SRC_GATHER)  // per-row push of k-1 colour partial sums through smem
                 mbytes += n * (double)(k - 1) * (double)st.cp * 4.0 * 0.1;
         }
