@@ -764,7 +764,9 @@ int launch_astep_vp(const Graph &g, const Plan &pl, const Step &st, const uint8_
             cudaDeviceGetAttribute(&v, cudaDevAttrL2CacheSize, dev);
             l2 = v > 0 ? v : (126ll << 20);
         }
-        const double H = 0.6 * (double)l2 / (double)(st.ldp * pl.elem);
+        static double hotfrac = -1;  // SG2V_HOTFRAC (experiments): share of L2 for hub rows
+        if (hotfrac < 0) { const char *e = getenv("SG2V_HOTFRAC"); hotfrac = e ? atof(e) : 0.6; }
+        const double H = hotfrac * (double)l2 / (double)(st.ldp * pl.elem);
         int hl = 0;
         while (hl < 31 && (double)(1ll << (hl + 1)) <= H) ++hl;
         A.hot_log2 = hl;
