@@ -31,6 +31,21 @@ def test_shard_covers_every_colouring_once():
             assert sorted(seen) == list(range(5, 5 + n))
 
 
+def test_vertex_partition_rows_tile_the_graph():
+    # contiguous row blocks, disjoint, covering [0, n) in rank order,
+    # at most ceil(n / world) rows each (n < world and n = 0 leave empty ranks)
+    from paper_2009_11665_b200.sg2v import partition_rows
+    for n in (0, 1, 2, 7, 8, 1000, 1 << 20):
+        for world in (1, 2, 3, 4, 8):
+            nxt = 0
+            for r in range(world):
+                b, nl = partition_rows(n, r, world)
+                assert nl >= 0 and nl <= -(-n // world)
+                assert b == nxt or nl == 0
+                nxt = b + nl if nl else nxt
+            assert nxt == n
+
+
 def _oracle_count_fn(case):
     from oracle import oracle as O
 
