@@ -267,9 +267,9 @@ static int32_t oracle_dp_##SUFFIX(int64_t n, const int64_t *rowptr, const int32_
     for (int32_t s = 0; s < t->n_nodes; ++s) {                                          \
         const oracle_node *nd = &t->nodes[s];                                           \
         int64_t cs = oracle_binom(k, nd->size);                                         \
-        M[s] = (T *)calloc((size_t)n * (size_t)cs + 1, sizeof(T));                      \
-        if (!M[s]) { rc = ORACLE_ENOMEM; break; }                                       \
         if (nd->active < 0) {                 /* leaf: P:183-188 */                     \
+            M[s] = (T *)calloc((size_t)n * (size_t)cs + 1, sizeof(T));                  \
+            if (!M[s]) { rc = ORACLE_ENOMEM; break; }                                   \
             for (int64_t i = 0; i < n; ++i)                                             \
                 M[s][(size_t)i * cs + rank[1u << colors[i]]] = 1;                       \
             if (TRACK_MAX && n > 0 && vmax < 1.0) vmax = 1.0;                           \
@@ -280,16 +280,22 @@ static int32_t oracle_dp_##SUFFIX(int64_t n, const int64_t *rowptr, const int32_
         int64_t ntr = 0;                                                                \
         int32_t *tr = oracle_splits(k, nd->size, na->size, rank, &ntr);                 \
         if (!tr) { rc = ORACLE_ENOMEM; break; }                                         \
-        const T *Ma = M[nd->active], *Mp = M[nd->passive];                              \
-        T *Ms = M[s];                                                                   \
+        const T *Ma = M[nd->active];                                                    \
         if (form == FORM_TWO_STAGE) {                                                   \
-            /* stage 1 (Alg. 3 l.1-4): B = A_G · M_p */                                \
+            /* stage 1 (Alg. 3 l.1-4): B = A_G · M_p.  M_p has no other reader, so it  \
+             * is freed before M_s is allocated (memory only: the host-RAM peak is     \
+             * max(|M_p|+|B|, |M_a|+|B|+|M_s|) instead of their sum; no arithmetic     \
+             * changes) */                                                              \
             T *B = (T *)malloc(sizeof(T) * ((size_t)n * (size_t)cp + 1));               \
             if (!B) { free(tr); rc = ORACLE_ENOMEM; break; }                            \
-            oracle_spmm_##SUFFIX(n, rowptr, col, Mp, cp, B);                            \
+            oracle_spmm_##SUFFIX(n, rowptr, col, M[nd->passive], cp, B);                \
             if (TRACK_MAX)                                                              \
                 for (size_t q = 0; q < (size_t)n * (size_t)cp; ++q)                     \
                     if ((double)B[q] > vmax) vmax = (double)B[q];                       \
+            free(M[nd->passive]); M[nd->passive] = NULL;                                \
+            M[s] = (T *)calloc((size_t)n * (size_t)cs + 1, sizeof(T));                  \
+            if (!M[s]) { free(B); free(tr); rc = ORACLE_ENOMEM; break; }                \
+            T *Ms = M[s];                                                               \
             /* stage 2 (Alg. 3 l.5-8): M_s(i,I_s) += M_a(i,I_a)·B(i,I_p) */           \
             _Pragma("omp parallel for schedule(dynamic, 64)")                           \
             for (int64_t i = 0; i < n; ++i)                                             \
@@ -299,6 +305,10 @@ static int32_t oracle_dp_##SUFFIX(int64_t n, const int64_t *rowptr, const int32_
                         B[(size_t)i * cp + tr[3 * w + 2]];                              \
             free(B);                                                                    \
         } else {                                                                        \
+            const T *Mp = M[nd->passive];                                               \
+            M[s] = (T *)calloc((size_t)n * (size_t)cs + 1, sizeof(T));                  \
+            if (!M[s]) { free(tr); rc = ORACLE_ENOMEM; break; }                         \
+            T *Ms = M[s];                                                               \
             /* literal Alg. 2 l.5-9: neighbour loop inside the split loop */           \
             _Pragma("omp parallel for schedule(dynamic, 64)")                           \
             for (int64_t i = 0; i < n; ++i)                                             \
@@ -311,7 +321,7 @@ static int32_t oracle_dp_##SUFFIX(int64_t n, const int64_t *rowptr, const int32_
         free(tr);                                                                       \
         if (TRACK_MAX)                                                                  \
             for (size_t q = 0; q < (size_t)n * (size_t)cs; ++q)                         \
-                if ((double)Ms[q] > vmax) vmax = (double)Ms[q];                         \
+                if ((double)M[s][q] > vmax) vmax = (double)M[s][q];                     \
         free(M[nd->active]);  M[nd->active] = NULL;  /* each child has one parent */  \
         free(M[nd->passive]); M[nd->passive] = NULL;                                    \
     }                                                                                   \
