@@ -167,6 +167,16 @@ sg2v_status sg2v_count_ex(const sg2v_graph *g, const sg2v_template *t, int32_t k
                           uint64_t *colorful_u64_out);
 
 /*
+ * sg2v_estimate — a7 for colourful counts gathered elsewhere (replica shards,
+ * SURVEY §8(e) R): estimate_out = (Σ_q colorful[q]) / n_iter / (P·α), summed in
+ * index order (deterministic), P = k!/k^k, α = |Aut(T)| of t (Alg. 1
+ * last line).  colorful: host double[n_iter] (F32/F64 counts).  EINVAL for NULL
+ * pointers or n_iter < 1; EOVERFLOW if a count is not finite (estimate written).
+ */
+sg2v_status sg2v_estimate(const sg2v_template *t, int64_t n_iter, const double *colorful,
+                          double *estimate_out);
+
+/*
  * sg2v_count_batch — m templates of the same size k on the SAME colourings
  * (treelet distributions, Fig. 1): the colouring and the
  * colour buckets / histogram are computed once per colouring and shared, then

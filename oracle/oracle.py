@@ -68,6 +68,9 @@ def lib():
         L.oracle_count.restype = i32
         L.oracle_count.argtypes = [i64, vp, vp, i32, vp, i32, vp, i32, i32,
                                    vp, vp, vp, vp, vp]
+        L.oracle_count_ex.restype = i32
+        L.oracle_count_ex.argtypes = [i64, vp, vp, i32, vp, i32, vp, i32, i32,
+                                      vp, vp, vp, vp, vp, vp]
         L.oracle_set_threads.restype = None
         L.oracle_set_threads.argtypes = [i32]
         L.oracle_get_threads.restype = i32
@@ -132,10 +135,13 @@ def ema(dst: np.ndarray, a: np.ndarray, b: np.ndarray) -> np.ndarray:
 
 
 def count(csr, k: int, edges, cols: np.ndarray, root: int = 0, form: int = FORM_TWO_STAGE,
-          arith: int = ARITH_U64, rows: bool = False):
+          arith: int = ARITH_U64, rows: bool = False, live: bool = False):
     """One colouring.  U64 -> int (mod 2^64); F64 -> (float, max_intermediate).
 
     With rows=True also returns the per-vertex values Σ_C M_0(i, I_C).
+    With live=True (F64) the tuple gains max_live after max_intermediate: the max over
+    every non-top table entry and every live B entry (I_p ∌ c(i)), the top's B
+    excluded when its active child is a leaf — the entries any F32 layout holds in F32.
     """
     n = csr.n
     if len(edges) != k - 1:
@@ -151,16 +157,19 @@ def count(csr, k: int, edges, cols: np.ndarray, root: int = 0, form: int = FORM_
     tot_u = np.zeros(1, np.uint64)
     tot_f = np.zeros(1, np.float64)
     vmax = np.zeros(1, np.float64)
+    vlive = np.zeros(1, np.float64)
     rows_u = np.zeros(max(n, 1), np.uint64) if (rows and arith == ARITH_U64) else None
     rows_f = np.zeros(max(n, 1), np.float64) if (rows and arith == ARITH_F64) else None
-    rc = lib().oracle_count(n, _ptr(ro), _ptr(ci), k, _ptr(e), root, _ptr(cols), form, arith,
-                            _ptr(tot_u), _ptr(rows_u) if rows_u is not None else None,
-                            _ptr(tot_f), _ptr(rows_f) if rows_f is not None else None, _ptr(vmax))
+    rc = lib().oracle_count_ex(n, _ptr(ro), _ptr(ci), k, _ptr(e), root, _ptr(cols), form, arith,
+                               _ptr(tot_u), _ptr(rows_u) if rows_u is not None else None,
+                               _ptr(tot_f), _ptr(rows_f) if rows_f is not None else None, _ptr(vmax),
+                               _ptr(vlive) if live else None)
     if rc != 0:
         raise ValueError({-1: "EINVAL", -2: "ENOTTREE", -3: "ENOMEM"}.get(rc, rc))
     if arith == ARITH_U64:
         return (int(tot_u[0]), rows_u[:n]) if rows else int(tot_u[0])
-    return (float(tot_f[0]), float(vmax[0]), rows_f[:n]) if rows else (float(tot_f[0]), float(vmax[0]))
+    head = (float(tot_f[0]), float(vmax[0])) + ((float(vlive[0]),) if live else ())
+    return head + (rows_f[:n],) if rows else head
 
 
 # ---------------------------------------------------------------------------

@@ -257,11 +257,13 @@ void oracle_ema_f64(int64_t len, double *dst, const double *a, const double *b)
 static int32_t oracle_dp_##SUFFIX(int64_t n, const int64_t *rowptr, const int32_t *col,  \
                                   const oracle_tpl *t, const int32_t *rank,             \
                                   const uint8_t *colors, int32_t form,                  \
-                                  T *out_total, T *out_rows, double *out_max)           \
+                                  T *out_total, T *out_rows, double *out_max,           \
+                                  double *out_max_live)                                 \
 {                                                                                       \
     int32_t k = t->k;                                                                   \
     T *M[2 * ORACLE_MAXK];                                                              \
-    double vmax = 0.0;                                                                  \
+    double vmax = 0.0, vlive = 0.0;                                                     \
+    const int32_t top = t->n_nodes - 1;                                                 \
     memset(M, 0, sizeof(M));                                                            \
     int32_t rc = ORACLE_OK;                                                             \
     for (int32_t s = 0; s < t->n_nodes; ++s) {                                          \
@@ -273,6 +275,7 @@ static int32_t oracle_dp_##SUFFIX(int64_t n, const int64_t *rowptr, const int32_
             for (int64_t i = 0; i < n; ++i)                                             \
                 M[s][(size_t)i * cs + rank[1u << colors[i]]] = 1;                       \
             if (TRACK_MAX && n > 0 && vmax < 1.0) vmax = 1.0;                           \
+            if (TRACK_MAX && n > 0 && s != top && vlive < 1.0) vlive = 1.0;             \
             continue;                                                                   \
         }                                                                               \
         const oracle_node *na = &t->nodes[nd->active], *np = &t->nodes[nd->passive];    \
@@ -292,6 +295,22 @@ static int32_t oracle_dp_##SUFFIX(int64_t n, const int64_t *rowptr, const int32_
             if (TRACK_MAX)                                                              \
                 for (size_t q = 0; q < (size_t)n * (size_t)cp; ++q)                     \
                     if ((double)B[q] > vmax) vmax = (double)B[q];                       \
+            /* live B entries: I_p avoids c(i) (else every product with M_a(i,.) is     \
+             * 0, M_a being 0 off c(i) ∈ I_a); the top's B is kept only when  \
+             * its active child is not a leaf (with a leaf, B(i,[k]\{c(i)}) is the       \
+             * per-vertex total itself) */                                              \
+            if (TRACK_MAX && out_max_live && (s != top || na->active >= 0)) {           \
+                uint32_t *mask_of = (uint32_t *)malloc(sizeof(uint32_t) * (size_t)cp);  \
+                if (!mask_of) { free(B); free(tr); rc = ORACLE_ENOMEM; break; }         \
+                for (uint32_t m = 0; m < (1u << k); ++m)                                \
+                    if (popc(m) == np->size) mask_of[rank[m]] = m;                      \
+                for (int64_t i = 0; i < n; ++i)                                         \
+                    for (int64_t q = 0; q < cp; ++q)                                    \
+                        if (!((mask_of[q] >> colors[i]) & 1u) &&                        \
+                            (double)B[(size_t)i * cp + q] > vlive)                      \
+                            vlive = (double)B[(size_t)i * cp + q];                      \
+                free(mask_of);                                                          \
+            }                                                                           \
             free(M[nd->passive]); M[nd->passive] = NULL;                                \
             M[s] = (T *)calloc((size_t)n * (size_t)cs + 1, sizeof(T));                  \
             if (!M[s]) { free(B); free(tr); rc = ORACLE_ENOMEM; break; }                \
@@ -322,12 +341,14 @@ static int32_t oracle_dp_##SUFFIX(int64_t n, const int64_t *rowptr, const int32_
         if (TRACK_MAX)                                                                  \
             for (size_t q = 0; q < (size_t)n * (size_t)cs; ++q)                         \
                 if ((double)M[s][q] > vmax) vmax = (double)M[s][q];                     \
+        if (TRACK_MAX && s != top)                                                      \
+            for (size_t q = 0; q < (size_t)n * (size_t)cs; ++q)                         \
+                if ((double)M[s][q] > vlive) vlive = (double)M[s][q];                   \
         free(M[nd->active]);  M[nd->active] = NULL;  /* each child has one parent */  \
         free(M[nd->passive]); M[nd->passive] = NULL;                                    \
     }                                                                                   \
     if (rc == ORACLE_OK) {                                                              \
         /* finalCount numerator: Σ_i Σ_C M_0(i,I_C); C(k,k) = 1 column */      \
-        int32_t top = t->n_nodes - 1;                                                   \
         T total = 0;                                                                    \
         for (int64_t i = 0; i < n; ++i) {                                               \
             T v = M[top][i];                                                            \
@@ -337,6 +358,7 @@ static int32_t oracle_dp_##SUFFIX(int64_t n, const int64_t *rowptr, const int32_
         if (TRACK_MAX && (double)total > vmax) vmax = (double)total;                    \
         *out_total = total;                                                             \
         if (out_max) *out_max = vmax;                                                   \
+        if (out_max_live) *out_max_live = vlive;                                        \
     }                                                                                   \
     for (int32_t s = 0; s < t->n_nodes; ++s) free(M[s]);                                \
     return rc;                                                                          \
@@ -348,13 +370,18 @@ ORACLE_DP(double, f64, 1)
  * One colouring.  colors[n] in [0,k) (from oracle_colors or any test colouring).
  * arith = ARITH_U64 writes *out_u64 (and out_rows_u64[n] if non-NULL);
  * arith = ARITH_F64 writes *out_f64, *out_max (and out_rows_f64[n]).
+ * oracle_count_ex also writes *out_max_live (F64, two-stage form): the max over the
+ * entries an F32 pipeline must hold in F32 whatever its layout — every non-top table
+ * entry and every live B entry (I_p ∌ c(i)) except the top's B when the top's active
+ * child is a leaf.  max_live > FLT_MAX means some stored F32 entry overflows.
  * Returns 0, or ORACLE_EINVAL / ORACLE_ENOTTREE / ORACLE_ENOMEM.
  */
-int32_t oracle_count(int64_t n, const int64_t *rowptr, const int32_t *col,
-                     int32_t k, const int32_t *edges, int32_t root,
-                     const uint8_t *colors, int32_t form, int32_t arith,
-                     uint64_t *out_u64, uint64_t *out_rows_u64,
-                     double *out_f64, double *out_rows_f64, double *out_max)
+int32_t oracle_count_ex(int64_t n, const int64_t *rowptr, const int32_t *col,
+                        int32_t k, const int32_t *edges, int32_t root,
+                        const uint8_t *colors, int32_t form, int32_t arith,
+                        uint64_t *out_u64, uint64_t *out_rows_u64,
+                        double *out_f64, double *out_rows_f64, double *out_max,
+                        double *out_max_live)
 {
     oracle_tpl t;
     int32_t rc = oracle_template(k, edges, root, &t);
@@ -364,11 +391,22 @@ int32_t oracle_count(int64_t n, const int64_t *rowptr, const int32_t *col,
     int32_t *rank = oracle_rank_table(k);
     if (!rank) return ORACLE_ENOMEM;
     if (arith == ARITH_U64)
-        rc = oracle_dp_u64(n, rowptr, col, &t, rank, colors, form, out_u64, out_rows_u64, NULL);
+        rc = oracle_dp_u64(n, rowptr, col, &t, rank, colors, form, out_u64, out_rows_u64, NULL, NULL);
     else
-        rc = oracle_dp_f64(n, rowptr, col, &t, rank, colors, form, out_f64, out_rows_f64, out_max);
+        rc = oracle_dp_f64(n, rowptr, col, &t, rank, colors, form, out_f64, out_rows_f64, out_max,
+                           out_max_live);
     free(rank);
     return rc;
+}
+
+int32_t oracle_count(int64_t n, const int64_t *rowptr, const int32_t *col,
+                     int32_t k, const int32_t *edges, int32_t root,
+                     const uint8_t *colors, int32_t form, int32_t arith,
+                     uint64_t *out_u64, uint64_t *out_rows_u64,
+                     double *out_f64, double *out_rows_f64, double *out_max)
+{
+    return oracle_count_ex(n, rowptr, col, k, edges, root, colors, form, arith, out_u64, out_rows_u64,
+                           out_f64, out_rows_f64, out_max, NULL);
 }
 
 void oracle_set_threads(int32_t nt)

@@ -132,12 +132,13 @@ struct AStepArgs {
     int tile_mode;      // stage 1 only: gather a staged column tile, push into bg rows
     int bsrc_global;    // stage 1 = copy the completed B row from bg
     char *bg;           // [n_local][ldb] B rows (tile_mode / bsrc_global)
+    int *ovf;           // F32 overflow flag of this sg2v_count call (in its workspace)
 };
 
-// F32 overflow flag: set by any anchored step that stores a non-finite table entry
-// (reset / read around every sg2v_count call; EOVERFLOW contract of sg2v.h).  Checked
-// at the stores, so the report does not depend on how inf / NaN propagate later.
-__device__ int g_ovf_flag;
+// F32 overflow flag (AStepArgs::ovf, one int in the calling sg2v_count's workspace, so
+// concurrent calls on other streams cannot clear or raise it): set by any step that
+// stores a non-finite table entry (EOVERFLOW contract of sg2v.h).  Checked at the
+// stores, so the report does not depend on how inf / NaN propagate later.
 
 template <typename T>
 __device__ __forceinline__ bool nonfinite(T x) {
@@ -350,8 +351,8 @@ __global__ void __launch_bounds__(256, AStepMinBlocks<U, V, MODE>::value) astep_
                         const T *a = reinterpret_cast<const T *>(A.ma) + (size_t)i * A.lda;
                         for (int64_t q = t; q < A.lda; q += GT) sBase[(A.ldb + q) * V + v] = __ldg(a + q);
                     }
-                } else {
-                    for (int64_t q = t; q < A.ldb + A.lda; q += GT) sBase[q * V + v] = 0;
+                } else {  // (only this slot's own entries: smem_group per row)
+                    for (int64_t q = t; q < A.smem_group; q += GT) sBase[q * V + v] = 0;
                 }
             }
             group_sync<GT>(g);
@@ -504,7 +505,7 @@ __global__ void __launch_bounds__(256, AStepMinBlocks<U, V, MODE>::value) astep_
         }
         group_sync<GT>(g);
     }
-    if (bad) atomicOr(&g_ovf_flag, 1);
+    if (bad) atomicOr(A.ovf, 1);
 }
 
 // ---------------------------------------------------------------------------
@@ -541,18 +542,12 @@ __global__ void __launch_bounds__(256) atop_leaf_kernel(int64_t n, int k, int kp
 // ---------------------------------------------------------------------------
 // launchers
 // ---------------------------------------------------------------------------
-int ovf_reset(void *stream) {
-    void *p = nullptr;
-    cudaError_t e = cudaGetSymbolAddress(&p, g_ovf_flag);
-    if (e != cudaSuccess) return (int)e;
-    return (int)cudaMemsetAsync(p, 0, sizeof(int), (cudaStream_t)stream);
+int ovf_reset(int *dflag, void *stream) {
+    return (int)cudaMemsetAsync(dflag, 0, sizeof(int), (cudaStream_t)stream);
 }
 
-int ovf_read(int *flag, void *stream) {
-    void *p = nullptr;
-    cudaError_t e = cudaGetSymbolAddress(&p, g_ovf_flag);
-    if (e != cudaSuccess) return (int)e;
-    e = cudaMemcpyAsync(flag, p, sizeof(int), cudaMemcpyDeviceToHost, (cudaStream_t)stream);
+int ovf_read(const int *dflag, int *flag, void *stream) {
+    cudaError_t e = cudaMemcpyAsync(flag, dflag, sizeof(int), cudaMemcpyDeviceToHost, (cudaStream_t)stream);
     if (e != cudaSuccess) return (int)e;
     return (int)cudaStreamSynchronize((cudaStream_t)stream);
 }
@@ -576,12 +571,7 @@ static int launch_astep_t(const AStepArgs &A, void *stream) {
     constexpr int G = 256 / GT;
     size_t smem = (size_t)G * V * A.smem_group * sizeof(T);
     if (smem > 227 * 1024) return -1;
-    static size_t configured = 0;
-    if (smem > 48 * 1024 && smem > configured) {
-        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        if (e != cudaSuccess) return (int)e;
-        configured = smem;
-    }
+    if (cudaError_t e = ensure_dyn_smem((const void *)kern, smem)) return (int)e;
     int occ = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 256, smem);
     if (occ < 1) occ = 1;
@@ -680,12 +670,12 @@ static int launch_astep_cfg(const AStepArgs &A0, void *stream) {
 }
 
 int launch_astep(const Graph &g, const Plan &pl, const Step &st, const uint8_t *colors, const int32_t *hcnt,
-                 const int32_t *bcol, char *tables, void *rowval, void *stream) {
-    return launch_astep_vp(g, pl, st, colors, hcnt, bcol, tables, rowval, stream, nullptr);
+                 const int32_t *bcol, char *tables, void *rowval, int *ovf, void *stream) {
+    return launch_astep_vp(g, pl, st, colors, hcnt, bcol, tables, rowval, ovf, stream, nullptr);
 }
 
 int launch_astep_vp(const Graph &g, const Plan &pl, const Step &st, const uint8_t *colors, const int32_t *hcnt,
-                    const int32_t *bcol, char *tables, void *rowval, void *stream, const VpArgs *vp) {
+                    const int32_t *bcol, char *tables, void *rowval, int *ovf, void *stream, const VpArgs *vp) {
     if (g.n <= 0) return 0;
     const int32_t *idx = pl.d_index + st.idx_off;
     const char *src = (st.src == SRC_HIST || (vp && vp->mode == 2)) ? nullptr : tables + pl.bufs[st.buf_p].offset;
@@ -747,6 +737,7 @@ int launch_astep_vp(const Graph &g, const Plan &pl, const Step &st, const uint8_
     A.tile_mode = 0;
     A.bsrc_global = 0;
     A.bg = nullptr;
+    A.ovf = ovf;
     // stage M_a next to B only while both fit comfortably (occupancy); else L1
     A.aoff = st.self_a ? 0 : st.ldb;
     static int stage_kb = -1;  // SG2V_STAGE_KB (experiments): M_a staging threshold

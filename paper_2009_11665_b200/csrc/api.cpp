@@ -189,8 +189,10 @@ static sg2v_status get_plan(int64_t n, int64_t nnz, int device, const Template &
         return SG2V_EINVAL;
     }
     const uint64_t budget = plan_budget(explicit_budget, device);
-    auto key = std::make_tuple((int)prec, n, nnz, device, (int)layout, budget);
-    auto &slot = const_cast<Template &>(t).plans[key];
+    auto key = std::make_tuple((int)prec, n, nnz, device, (int)layout, budget, (int64_t)0);
+    Template &tm = const_cast<Template &>(t);
+    std::lock_guard<std::mutex> plan_lock(tm.mu);  // plan cache + lazy index upload
+    auto &slot = tm.plans[key];
     if (!slot) {
         std::unique_ptr<Plan> pl;
         sg2v_status st = make_plan(t, n, nnz, prec, current_layout(layout), budget, pl, 0, 0,
@@ -404,7 +406,7 @@ namespace sg2v {
 // is exactly the plan's own layout (Plan::ws_bytes).
 struct BatchLayout {
     int64_t off_colors = 0, off_hist = 0, off_hcnt = 0, off_bcol = 0, off_rowval = 0, off_partial = 0,
-            off_results = 0, bytes = 0;
+            off_results = 0, off_flag = 0, bytes = 0;
 };
 
 static int64_t rup(int64_t x, int64_t m) { return (x + m - 1) / m * m; }
@@ -427,6 +429,7 @@ static BatchLayout batch_layout(const std::vector<Plan *> &pls, int64_t n, int64
     L.off_rowval = off;  off = rup(off + std::max<int64_t>(n, 1) * 8, 256);
     L.off_partial = off; off = rup(off + kReduceBlocks * 8, 256);
     L.off_results = off; off = rup(off + (int64_t)kResultsRing * 8 * (int64_t)std::max<size_t>(pls.size(), 1), 256);
+    L.off_flag = off;    off = rup(off + 16, 256);
     L.bytes = off;
     return L;
 }
@@ -572,14 +575,15 @@ static sg2v_status count_vp(const sg2v_graph *g, const sg2v_template *t, int32_t
     std::vector<double> resf(n_iter, 0.0);
     std::vector<uint64_t> resu(n_iter, 0);
     int ovf = 0;
-    if (!u64mode && k > 1) SG2V_CK((cudaError_t)ovf_reset(s));
     if (k == 1) {
         for (int64_t q = 0; q < n_iter; ++q) { resf[q] = (double)n_global; resu[q] = (uint64_t)n_global; }
     } else {
         // plan on the local rows; staging sized for world·nl global rows
         auto key = std::make_tuple((int)o.precision, g->n, g->nnz, -(g->device + 1) - 1000 * c->world, 0,
-                                   (uint64_t)o.col_tile);
-        auto &slot = const_cast<Template &>(*(const Template *)t).plans[key];
+                                   (uint64_t)o.col_tile, (int64_t)c->world * nl);
+        Template &tm = const_cast<Template &>(*(const Template *)t);
+        std::unique_lock<std::mutex> plan_lock(tm.mu);
+        auto &slot = tm.plans[key];
         if (!slot) {
             std::unique_ptr<Plan> pl;
             st = make_plan(*t, std::max<int64_t>(g->n, 1), std::max<int64_t>(g->nnz, 1), o.precision, LAYOUT_ANCHORED,
@@ -592,6 +596,7 @@ static sg2v_status count_vp(const sg2v_graph *g, const sg2v_template *t, int32_t
             SG2V_CK(cudaMalloc(&pl->d_index, pl->index.size() * sizeof(int32_t)));
             SG2V_CK(cudaMemcpy(pl->d_index, pl->index.data(), pl->index.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
         }
+        plan_lock.unlock();
         char *ws = (char *)o.workspace;
         bool own = false;
         if (ws) {
@@ -612,6 +617,8 @@ static sg2v_status count_vp(const sg2v_graph *g, const sg2v_template *t, int32_t
         void *rowval = ws + pl->off_rowval;
         void *partial = ws + pl->off_partial;
         char *part = ws + pl->off_part;  // [0]: this rank's Σ_i, [8..]: all ranks'
+        int *dflag = (int *)(ws + pl->off_flag);
+        if (!u64mode) SG2V_CK((cudaError_t)ovf_reset(dflag, s));
         const int64_t E = pl->elem, W = pl->tile_w;
         const int vn = 16 / pl->elem;
         std::vector<uint64_t> hpart(c->world);
@@ -623,7 +630,7 @@ static sg2v_status count_vp(const sg2v_graph *g, const sg2v_template *t, int32_t
             int par = 0;
             for (const Step &stp : pl->steps) {
                 if (stp.src == SRC_HIST) {  // local (the histogram is local)
-                    rc = launch_astep_vp(*g, *pl, stp, colors_l, hcnt, bcol, ws, rowval, s, nullptr);
+                    rc = launch_astep_vp(*g, *pl, stp, colors_l, hcnt, bcol, ws, rowval, dflag, s, nullptr);
                     if (rc) return cuda_fail("step", rc == -1 ? 0 : rc);
                     continue;
                 }
@@ -647,7 +654,7 @@ static sg2v_status count_vp(const sg2v_graph *g, const sg2v_template *t, int32_t
                     va.u0 = u0;
                     va.cnt = cnt;
                     va.bg = bg;
-                    rc = launch_astep_vp(*g, *pl, stp, colors_l, hcnt, bcol, ws, rowval, s, &va);
+                    rc = launch_astep_vp(*g, *pl, stp, colors_l, hcnt, bcol, ws, rowval, dflag, s, &va);
                     if (rc) return cuda_fail("tile", rc == -1 ? 0 : rc);
                     par ^= 1;
                 }
@@ -658,7 +665,7 @@ static sg2v_status count_vp(const sg2v_graph *g, const sg2v_template *t, int32_t
                     VpArgs va;
                     va.mode = 2;
                     va.bg = bg;
-                    rc = launch_astep_vp(*g, *pl, stp, colors_l, hcnt, bcol, ws, rowval, s, &va);
+                    rc = launch_astep_vp(*g, *pl, stp, colors_l, hcnt, bcol, ws, rowval, dflag, s, &va);
                 }
                 if (rc) return cuda_fail("combine", rc == -1 ? 0 : rc);
             }
@@ -683,7 +690,7 @@ static sg2v_status count_vp(const sg2v_graph *g, const sg2v_template *t, int32_t
             resu[q] = su;
             resf[q] = sf;
         }
-        if (!u64mode) SG2V_CK((cudaError_t)ovf_read(&ovf, s));
+        if (!u64mode) SG2V_CK((cudaError_t)ovf_read(dflag, &ovf, s));
     }
     bool finite = ovf == 0;  // a stored F32 table entry overflowed on this rank
     double sum = 0.0;
@@ -786,12 +793,13 @@ static sg2v_status count_core(const sg2v_graph *g, const sg2v_template *const *t
         char *results = ws + L.off_results;
         int32_t *hcnt = (int32_t *)(ws + L.off_hcnt);
         int32_t *bcol = (int32_t *)(ws + L.off_bcol);
+        int *dflag = (int *)(ws + L.off_flag);
         const bool anch = pls[0]->layout == LAYOUT_ANCHORED;
         bool need_hist = false;
         for (Plan *p : pls) need_hist = need_hist || p->need_hist;
         std::vector<uint64_t> host_ring((size_t)kResultsRing * m);
         int64_t base = 0;
-        if (!u64mode) SG2V_CK((cudaError_t)ovf_reset(s));
+        if (!u64mode) SG2V_CK((cudaError_t)ovf_reset(dflag, s));
         for (int64_t q = 0; q < n_iter; ++q) {
             const int64_t j = o.iter_offset + q * o.iter_stride;
             int rc = launch_colorize(seed, j, g->n, k, colors, s);
@@ -801,8 +809,8 @@ static sg2v_status count_core(const sg2v_graph *g, const sg2v_template *const *t
             for (int32_t tq = 0; tq < m; ++tq) {
                 const Plan *pl = pls.size() > 1 ? &J.views[tq] : pls[tq];
                 for (const Step &stp : pl->steps) {
-                    rc = anch ? launch_astep(*g, *pl, stp, colors, hcnt, bcol, ws, rowval, s)
-                              : launch_step(*g, *pl, stp, colors, H, ws, rowval, s);
+                    rc = anch ? launch_astep(*g, *pl, stp, colors, hcnt, bcol, ws, rowval, dflag, s)
+                              : launch_step(*g, *pl, stp, colors, H, ws, rowval, dflag, s);
                     if (rc == -1) {
                         set_error("row too wide for on-chip B (shared memory > 227 KB)");
                         return SG2V_ENOMEM;
@@ -830,7 +838,7 @@ static sg2v_status count_core(const sg2v_graph *g, const sg2v_template *const *t
             SG2V_CK(cudaMemcpyAsync(o.row_values, rowval, g->n * 8, cudaMemcpyDeviceToDevice, s));
             SG2V_CK(cudaStreamSynchronize(s));
         }
-        if (!u64mode && anch) SG2V_CK((cudaError_t)ovf_read(&ovf, s));
+        if (!u64mode) SG2V_CK((cudaError_t)ovf_read(dflag, &ovf, s));
     }
     bool finite = ovf == 0;  // a stored F32 table entry overflowed (set by the step kernels)
     for (int32_t tq = 0; tq < m; ++tq) {
@@ -884,6 +892,19 @@ sg2v_status sg2v_workspace_bytes_batch(const sg2v_graph *g, const sg2v_template 
     JointPlan J;
     if (pls.size() > 1) joint_schedule(pls, J);
     *bytes = pls.empty() ? 0 : (uint64_t)batch_layout(pls, g->n, g->nnz, pls.size() > 1 ? J.tables_bytes : -1).bytes;
+    return SG2V_OK;
+}
+
+sg2v_status sg2v_estimate(const sg2v_template *t, int64_t n_iter, const double *colorful, double *estimate_out) {
+    if (!t || !colorful || !estimate_out || n_iter < 1) { set_error("bad argument"); return SG2V_EINVAL; }
+    double sum = 0.0;
+    bool finite = true;
+    for (int64_t q = 0; q < n_iter; ++q) {
+        finite = finite && std::isfinite(colorful[q]);
+        sum += colorful[q];
+    }
+    *estimate_out = sum / (double)n_iter / (t->P * t->alpha);
+    if (!finite) { set_error("EOVERFLOW: a colourful count is not finite"); return SG2V_EOVERFLOW; }
     return SG2V_OK;
 }
 

@@ -4,6 +4,9 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <map>
+#include <mutex>
+#include <utility>
 
 namespace sg2v {
 
@@ -138,5 +141,22 @@ __device__ __forceinline__ void vset(uint4 &v, int e, T x) {
 }
 
 int num_sms();
+
+// Opt a kernel into `smem` bytes of dynamic shared memory on the CURRENT device.
+// The attribute is per (function, device), so it is tracked per (kernel, device)
+// under a lock (launches may come from several threads / devices).
+inline cudaError_t ensure_dyn_smem(const void *kern, size_t smem) {
+    if (smem <= 48 * 1024) return cudaSuccess;
+    static std::mutex mu;
+    static std::map<std::pair<const void *, int>, size_t> done;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> lk(mu);
+    size_t &have = done[{kern, dev}];
+    if (have >= smem) return cudaSuccess;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e == cudaSuccess) have = smem;
+    return e;
+}
 
 }  // namespace sg2v

@@ -19,6 +19,7 @@
 #include <cub/cub.cuh>
 
 #include <cstdio>
+#include <type_traits>
 
 #include "kcommon.cuh"
 #include "sg2v_internal.h"
@@ -92,6 +93,7 @@ struct StepArgs {
     int64_t nterms;
     void *rowval;      // top: per-vertex values (RT)
     int64_t smem_group;  // elements of shared memory per row group
+    int *ovf;          // F32 overflow flag of the call (workspace)
 };
 
 template <typename T, typename RT, int GT>
@@ -108,6 +110,7 @@ __global__ void __launch_bounds__(256) step_kernel(StepArgs A) {
     const int64_t nslots = (A.n + G - 1) / G;
     const int64_t nvec = A.ldp / VN;
     const size_t row_bytes = (size_t)A.ldp * sizeof(T);
+    bool bad = false;  // a stored F32 table entry is not finite (EOVERFLOW)
 
     for (int64_t slot = blockIdx.x; slot < nslots; slot += gridDim.x) {
         const int64_t r = slot * G + g;
@@ -177,6 +180,7 @@ __global__ void __launch_bounds__(256) step_kernel(StepArgs A) {
                             const int32_t q = __ldg(m + o);
                             if (q >= 0) val = sB[q];
                         }
+                        if constexpr (std::is_same<T, float>::value) bad |= !isfinite(val);
                         out[o] = val;
                     }
                 } else {
@@ -190,6 +194,7 @@ __global__ void __launch_bounds__(256) step_kernel(StepArgs A) {
                                 acc += sA[q.x] * sB[q.y];
                             }
                         }
+                        if constexpr (std::is_same<T, float>::value) bad |= !isfinite(acc);
                         out[o] = acc;
                     }
                 }
@@ -207,6 +212,7 @@ __global__ void __launch_bounds__(256) step_kernel(StepArgs A) {
         }
         group_sync<GT>(g);
     }
+    if (bad) atomicOr(A.ovf, 1);
 }
 
 // ---------------------------------------------------------------------------
@@ -352,13 +358,7 @@ static int launch_step_t(const StepArgs &A, void *stream) {
     constexpr int G = 256 / GT;
     size_t smem = (size_t)G * A.smem_group * sizeof(T);
     if (smem > 227 * 1024) return -1;
-    static size_t configured = 0;
-    if (smem > 48 * 1024 && smem > configured) {
-        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        if (e != cudaSuccess) return (int)e;
-        configured = smem;
-    }
-    int occ = 0;
+    if (cudaError_t e = ensure_dyn_smem((const void *)kern, smem)) return (int)e;    int occ = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 256, smem);
     if (occ < 1) occ = 1;
     int64_t nslots = (A.n + G - 1) / G;
@@ -382,7 +382,7 @@ static int launch_step_gt(const StepArgs &A, int gt, void *stream) {
 }
 
 int launch_step(const Graph &g, const Plan &pl, const Step &st, const uint8_t *colors, const void *H,
-                char *tables, void *rowval, void *stream) {
+                char *tables, void *rowval, int *ovf, void *stream) {
     if (g.n <= 0) return 0;
     const int32_t *idx = pl.d_index + st.idx_off;
     const char *src = (st.src == SRC_HIST) ? (const char *)H : tables + pl.bufs[st.buf_p].offset;
@@ -423,6 +423,7 @@ int launch_step(const Graph &g, const Plan &pl, const Step &st, const uint8_t *c
     A.nterms = st.nterms;
     A.rowval = rowval;
     A.smem_group = st.ldp + (st.comb == COMB_GENERAL ? st.lda : 0);
+    A.ovf = ovf;
     int cls = st.top ? 3 : 2;
     prof_begin(cls, stream);
     int rc;

@@ -507,6 +507,7 @@ static bool plan_chain(const Template &t, const Chain &c, int root, int64_t n, i
     pl.off_rowval = off;  off = round_up(off + std::max<int64_t>(n, 1) * 8, 256);
     pl.off_partial = off; off = round_up(off + kReduceBlocks * 8, 256);
     pl.off_results = off; off = round_up(off + kResultsRing * 8, 256);
+    pl.off_flag = off;    off = round_up(off + 16, 256);
     pl.ws_bytes = off;
     return true;
 }

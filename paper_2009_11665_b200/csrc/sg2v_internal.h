@@ -6,6 +6,7 @@
 #include <cstdint>
 #include <map>
 #include <memory>
+#include <mutex>
 #include <set>
 #include <string>
 #include <tuple>
@@ -101,7 +102,7 @@ struct Plan {
     std::vector<Buffer> bufs;     // count tables (offsets inside the workspace)
     int64_t tables_bytes = 0;     // peak of the table arena
     int64_t kp = 0;               // anchored: hcnt row stride (int32 colour counts)
-    int64_t off_colors = 0, off_hist = 0, off_rowval = 0, off_partial = 0, off_results = 0;
+    int64_t off_colors = 0, off_hist = 0, off_rowval = 0, off_partial = 0, off_results = 0, off_flag = 0;
     int64_t off_hcnt = 0, off_bcol = 0;   // anchored: colour counts + colour-bucketed CSR
     // vertex-partitioned mode: rows are local (n = n_local), colours/staging are global
     bool vp = false;
@@ -133,7 +134,9 @@ struct Template {
     std::vector<std::vector<int>> adj;
     double alpha = 1.0;
     double P = 1.0;
-    std::map<std::tuple<int, int64_t, int64_t, int, int, uint64_t>, std::unique_ptr<Plan>> plans;
+    // (precision, n, nnz, device | vertex-mode tag, layout, budget | col_tile, vertex-mode staging rows)
+    std::map<std::tuple<int, int64_t, int64_t, int, int, uint64_t, int64_t>, std::unique_ptr<Plan>> plans;
+    std::mutex mu;  // guards plans and the lazy index upload (handles may be shared by threads)
     ~Template();
 };
 
@@ -152,16 +155,17 @@ int launch_hist(const Graph &g, const Plan &pl, const uint8_t *colors, void *H, 
 int launch_bucket(const Graph &g, const Plan &pl, const uint8_t *colors, int32_t *hcnt, int32_t *bcol,
                   void *stream);
 int launch_astep(const Graph &g, const Plan &pl, const Step &st, const uint8_t *colors, const int32_t *hcnt,
-                 const int32_t *bcol, char *tables, void *rowval, void *stream);
+                 const int32_t *bcol, char *tables, void *rowval, int *ovf, void *stream);
 int launch_astep_vp(const Graph &g, const Plan &pl, const Step &st, const uint8_t *colors, const int32_t *hcnt,
-                    const int32_t *bcol, char *tables, void *rowval, void *stream, const VpArgs *vp);
-int ovf_reset(void *stream);             // F32 overflow flag of the anchored steps
-int ovf_read(int *flag, void *stream);
+                    const int32_t *bcol, char *tables, void *rowval, int *ovf, void *stream, const VpArgs *vp);
+// F32 overflow flag of one sg2v_count call: a device int inside its workspace
+int ovf_reset(int *dflag, void *stream);
+int ovf_read(const int *dflag, int *flag, void *stream);
 int launch_pack_tile(int64_t n, const char *src, int64_t ld_bytes, int64_t u0_bytes, int64_t w_bytes, char *dst,
                      int64_t dst_ld_bytes, void *stream);
 int launch_bg_rowval(const Plan &pl, int64_t n, const char *bg, int64_t ldb, void *rowval, void *stream);
 int launch_step(const Graph &g, const Plan &pl, const Step &st, const uint8_t *colors,
-                const void *H, char *tables, void *rowval, void *stream);
+                const void *H, char *tables, void *rowval, int *ovf, void *stream);
 int launch_reduce(const Plan &pl, int64_t n, const void *rowval, void *partial, void *result,
                   void *stream);
 int graph_build_order(Graph &g, void *stream);

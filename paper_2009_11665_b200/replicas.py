@@ -62,6 +62,7 @@ def count_replicated(graph, tmpl, n_iter: int, seed: int, precision: str = "f32"
     full = gather_counts(local, n_iter, rank, world, precision, device=device, group=group)
     if precision == "u64":
         return float("nan"), full
-    info = tmpl.info() if hasattr(tmpl, "info") else tmpl
-    est = float(np.mean(full)) / (info["P"] * info["alpha"]) if n_iter else float("nan")
-    return est, full
+    if not n_iter:
+        return float("nan"), full
+    from .sg2v import estimate  # a7 (mean / (P·α)) runs in the C ABI: sg2v_estimate
+    return estimate(tmpl, full), full

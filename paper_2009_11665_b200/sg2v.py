@@ -55,7 +55,7 @@ SYMBOLS = ["sg2v_graph_load_csr", "sg2v_graph_free", "sg2v_template_build", "sg2
            "sg2v_count", "sg2v_count_ex", "sg2v_colorize", "sg2v_plan_describe", "sg2v_plan_describe_n", "sg2v_profile_enable",
            "sg2v_profile_read", "sg2v_last_error", "sg2v_version", "sg2v_count_batch",
            "sg2v_workspace_bytes_batch", "sg2v_comm_unique_id", "sg2v_comm_init_nccl", "sg2v_comm_init_callback",
-           "sg2v_comm_free", "sg2v_graph_load_partition"]
+           "sg2v_comm_free", "sg2v_graph_load_partition", "sg2v_estimate"]
 
 ALLGATHER_FN = ctypes.CFUNCTYPE(ctypes.c_int32, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_uint64, ctypes.c_void_p)
 
@@ -94,6 +94,7 @@ def lib():
         L.sg2v_workspace_bytes_batch.argtypes = [vp, vp, i32, ctypes.c_int, P(u64)]
         L.sg2v_plan_describe.argtypes = [vp, vp, ctypes.c_int, vp, u64, P(u64)]
         L.sg2v_plan_describe_n.argtypes = [i64, i64, vp, ctypes.c_int, vp, u64, P(u64)]
+        L.sg2v_estimate.argtypes = [vp, i64, vp, P(ctypes.c_double)]
         L.sg2v_profile_enable.argtypes = [i32]
         L.sg2v_profile_read.argtypes = [vp, vp, vp]
         L.sg2v_last_error.restype = ctypes.c_char_p
@@ -102,7 +103,8 @@ def lib():
                      "sg2v_workspace_bytes", "sg2v_count", "sg2v_count_ex", "sg2v_colorize",
                      "sg2v_plan_describe", "sg2v_plan_describe_n", "sg2v_profile_enable", "sg2v_profile_read",
                      "sg2v_count_batch", "sg2v_workspace_bytes_batch", "sg2v_comm_unique_id",
-                     "sg2v_comm_init_nccl", "sg2v_comm_init_callback", "sg2v_graph_load_partition"):
+                     "sg2v_comm_init_nccl", "sg2v_comm_init_callback", "sg2v_graph_load_partition",
+                     "sg2v_estimate"):
             getattr(L, name).restype = ctypes.c_int
         _lib = L
     return _lib
@@ -315,6 +317,16 @@ def count(graph: Graph, tmpl: Template, n_iter: int, seed: int, precision="f32",
         return est.value, out
     _check(rc)
     return est.value, out
+
+
+def estimate(tmpl: Template, colorful) -> float:
+    """sg2v_estimate: mean/(P·α) of host per-colouring counts (replica shards)."""
+    c = np.ascontiguousarray(colorful, dtype=np.float64)
+    est = ctypes.c_double()
+    rc = lib().sg2v_estimate(tmpl.handle, int(c.size), c.ctypes.data, ctypes.byref(est))
+    if rc != EOVERFLOW:
+        _check(rc)
+    return est.value
 
 
 def _handles(tmpls):

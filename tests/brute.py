@@ -67,3 +67,51 @@ def injective_homs(csr, k, edges, colors=None):
 
     rec(0)
     return total
+
+
+def automorphisms_backtrack(k, edges, cap=None):
+    """|Aut(T)| of an (unrooted) tree by explicit enumeration: every bijection
+    V_T -> V_T that maps edges to edges, built vertex by vertex in BFS
+    order (each vertex after the first must land on a neighbour of its parent's
+    image, degrees must match).  Independent of the AHU product formula.  Returns
+    None if more than `cap` automorphisms exist (too many to list)."""
+    adj = [set() for _ in range(k)]
+    for a, b in edges:
+        adj[a].add(b)
+        adj[b].add(a)
+    deg = [len(x) for x in adj]
+    order, parent, seen = [0], {0: -1}, {0}
+    i = 0
+    while i < len(order):
+        for w in sorted(adj[order[i]]):
+            if w not in seen:
+                seen.add(w)
+                parent[w] = order[i]
+                order.append(w)
+        i += 1
+    phi = [-1] * k
+    used = [False] * k
+    count = 0
+
+    def rec(t):
+        nonlocal count
+        if cap is not None and count > cap:
+            return
+        if t == k:
+            count += 1
+            return
+        v = order[t]
+        cand = range(k) if parent[v] < 0 else adj[phi[parent[v]]]
+        for x in cand:
+            if used[x] or deg[x] != deg[v]:
+                continue
+            if any(phi[u] >= 0 and (phi[u] in adj[x]) != (u in adj[v]) for u in range(k)):
+                continue
+            phi[v] = x
+            used[x] = True
+            rec(t + 1)
+            used[x] = False
+            phi[v] = -1
+
+    rec(0)
+    return None if (cap is not None and count > cap) else count

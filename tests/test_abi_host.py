@@ -187,3 +187,17 @@ def test_dual_tables_for_classes_read_as_active_and_passive():
     assert (top["s"], top["a"], top["p"]) == (12, 6, 6) and top["proj_p"] and top["cp"] == math.comb(10, 5)
     prod = [s for s in d["steps"] if s["s"] == 6 and not s["top"]][0]
     assert prod["proj_out"] and prod["plain_out"]
+
+
+def test_library_alpha_matches_enumeration():
+    """α of the library's planner (AHU, planner.cpp) against explicit enumeration of the
+    automorphism group (tests/brute.py) for every repo template whose group is listable
+    (u10..u20 included), and (k-1)! for stars — independent of the oracle's AHU too."""
+    from tests.brute import automorphisms_backtrack
+    for name, e in TEMPLATES.items():
+        k = 1 + max(max(x) for x in e) if e else 1
+        a = automorphisms_backtrack(k, e, cap=50_000) if e else 1
+        if a is None:
+            assert name.startswith("star")
+            a = math.factorial(k - 1)
+        assert sg.template_build(k, e).info()["alpha"] == a, name

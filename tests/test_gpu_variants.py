@@ -85,3 +85,51 @@ def test_knob_configuration_vs_oracle(want, knob):
             assert got[f"{name}/{layout}/u64"] == wu, (knob, name, layout)
             f32 = got[f"{name}/{layout}/f32"]
             assert math.isclose(f32, wf, rel_tol=1e-4), (knob, name, layout, f32, wf)
+
+
+# n % (row-group rows) != 0 with M_a not staged (SG2V_STAGE_KB=0) and the V-row eMA variants
+# (V = 2/4 rows per group, GENERAL steps with many split terms): the inactive tail rows of
+# the last slot must stay inside the block's shared memory (the zero-fill of
+# an inactive row once ran past it).  Per-vertex values in U64 against the oracle.
+_TAIL_SCRIPT = r"""
+import sys, numpy as np, torch
+import paper_2009_11665_b200 as sg
+from sg2v_inputs import TEMPLATES, erdos_renyi
+torch.cuda.set_device(0)
+g = erdos_renyi(1001, 6000, seed=17)
+G = sg.graph_load_csr(g.n, g.row_offsets, g.col_indices, validate=True)
+out = {}
+for name in sys.argv[1].split(","):
+    e = TEMPLATES[name]; k = 1 + max(max(x) for x in e)
+    T = sg.template_build(k, e)
+    for layout in ("anchored", "anchored_plain"):
+        rv = torch.zeros(g.n, dtype=torch.int64, device="cuda")
+        _, c = sg.count(G, T, n_iter=1, seed=3, precision="u64", row_values=rv, layout=layout)
+        out[f"{name}/{layout}"] = rv.cpu().numpy().view(np.uint64)
+        out[f"{name}/{layout}/root"] = np.array([sg.plan_describe(G, T, "u64", layout)["root"]])
+np.savez(sys.argv[2], **{k.replace("/", "__"): v for k, v in out.items()})
+"""
+
+
+@pytest.mark.parametrize("stage_kb", ["0", "100"])
+def test_ragged_tail_rows_vrow_variants(oracle, tmp_path, stage_kb):
+    import numpy as np
+    from sg2v_inputs import erdos_renyi
+    names = ("star17", "u17-s22", "u14-2", "star12")
+    f = tmp_path / "rows.npz"
+    env = dict(os.environ, SG2V_STAGE_KB=stage_kb)
+    p = subprocess.run([sys.executable, "-c", _TAIL_SCRIPT, ",".join(names), str(f)],
+                       cwd=ROOT, env=env, capture_output=True, text=True, timeout=900)
+    assert p.returncode == 0, p.stderr[-2000:]
+    got = np.load(f)
+    g = erdos_renyi(1001, 6000, seed=17)
+    for name in names:
+        e = TEMPLATES[name]
+        k = 1 + max(max(x) for x in e)
+        cols = oracle.colors(3, 0, g.n, k)
+        for layout in ("anchored", "anchored_plain"):
+            rho = int(got[f"{name}__{layout}__root"][0])
+            want_tot, want_rows = oracle.count(g, k, e, cols, root=rho, rows=True)
+            r = got[f"{name}__{layout}"]
+            assert np.array_equal(r, want_rows), (name, layout, stage_kb)
+            assert int(r.sum(dtype=np.uint64)) == want_tot

@@ -5,7 +5,7 @@
   single-GPU path (U64 exact, F64 below 2^53 exact, F32 1e-4).
 * world = 2 with two processes sharing cuda:0 and the host-callback transport over
   gloo: each rank holds half of the rows of every table; the all-gathered counts
-  must equal the single-process values bit-exactly (U64).
+  must equal the single-process values bit-exactly (U64) AND the CPU oracle's.
 """
 import os
 import socket
@@ -39,7 +39,7 @@ def _dev():
 
 
 @pytest.mark.parametrize("name", ["u3-1", "u5-2", "u7-2", "path6", "star6", "u10-2"])
-def test_world1_nccl_tiled_equals_single(name):
+def test_world1_nccl_tiled_equals_single(oracle, name):
     g = rmat(12, 60_000, 0.45, 0.22, 0.22, seed=6)
     e = TEMPLATES[name]
     k = _k(e)
@@ -56,6 +56,11 @@ def test_world1_nccl_tiled_equals_single(name):
         _, wf = sg.count(G, T, n_iter=2, seed=2, precision="f32")
         _, gf = sg.count(Gp, T, n_iter=2, seed=2, precision="f32", comm=comm, col_tile=8)
         assert np.allclose(gf, wf, rtol=1e-4, atol=0)
+        # and against the oracle directly (U64 residues, F64 values for the F32 bar)
+        for j in range(2):
+            cols = oracle.colors(2, j, g.n, k)
+            assert int(want[j]) == oracle.count(g, k, e, cols)
+            assert abs(gf[j] - oracle.count(g, k, e, cols, arith=oracle.ARITH_F64)[0]) <= 1e-4 * abs(gf[j])
     comm.free()
 
 
@@ -97,7 +102,7 @@ def _worker(rank, world, port, q):
     q.put((rank, res))
 
 
-def test_world2_callback_equals_single():
+def test_world2_callback_equals_single(oracle):
     import torch.multiprocessing as mp
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
@@ -115,3 +120,5 @@ def test_world2_callback_equals_single():
         e = TEMPLATES[name]
         _, want = sg.count(G, sg.template_build(_k(e), e), n_iter=2, seed=5, precision="u64")
         assert out[0][name] == [int(x) for x in want] == out[1][name], name
+        k = _k(e)
+        assert out[0][name] == [oracle.count(g, k, e, oracle.colors(5, j, g.n, k)) for j in range(2)], name

@@ -312,3 +312,51 @@ def test_u64_matches_f64_below_2_53(oracle):
         u = oracle.count(g, k, e, cols)
         f, vmax = oracle.count(g, k, e, cols, arith=oracle.ARITH_F64)
         assert vmax < 2 ** 53 and f == float(u)
+
+
+# --------------------------------------------------------------------------- α beyond brute-force k! (k = 9, 10, repo templates)
+def test_alpha_ahu_vs_enumeration(oracle):
+    """The oracle's α for k >= 9 comes from the AHU product formula; pin it against
+    explicit enumeration of the automorphisms (tests/brute.py, backtracking, no AHU)
+    for random trees with k = 9, 10 and every repo template whose group is listable,
+    and against the closed form |Aut(S_k)| = (k-1)! for stars (k >= 3)."""
+    from sg2v_inputs import TEMPLATES
+    from tests.brute import automorphisms_backtrack
+    cases = [(k, random_tree(k, 1000 * k + s)) for k in (9, 10) for s in range(8)]
+    cases += [(1 + max(max(x) for x in e), e) for name, e in TEMPLATES.items()
+              if e and not name.startswith("star")]
+    checked = 0
+    for k, e in cases:
+        a = automorphisms_backtrack(k, e, cap=50_000)
+        if a is None:
+            continue
+        assert oracle.alpha_ahu(k, e) == a, (k, e)
+        assert oracle.alpha(k, e) == a
+        checked += 1
+    assert checked >= len(cases) - 2
+    for k in range(3, 21):
+        assert oracle.alpha_ahu(k, star_template(k)) == math.factorial(k - 1)
+
+
+# --------------------------------------------------------------------------- max-intermediate gates
+def test_max_intermediate_includes_B_and_live_max_excludes_dead(oracle):
+    """vmax (the "exact below 2^53 / 2^24" gate, SURVEY §8(c) pin 6) must include the
+    B = A·M_p entries, and max_live (the F32-overflow gate) must leave out the B entries
+    that only meet zeros (I_p ∋ c(i)) and a leaf-active top's B.  Crafted on the star
+    K_{1,m} (centre 0) with closed-form values."""
+    m = 7
+    g = _graph(m + 1, [(0, x) for x in range(1, m + 1)])
+    # monochromatic: colorful = 0, every table entry <= 1, but B(centre,{0}) = m
+    tot, vmax, live = oracle.count(g, 2, [(0, 1)], np.zeros(m + 1, np.uint8), arith=oracle.ARITH_F64, live=True)
+    assert (tot, vmax, live) == (0.0, float(m), 1.0)
+    # centre colour 0, leaves colour 1: colorful = 2m (both orientations), leaf tables = 1,
+    # the top's B(i,[k]\{c(i)}) = per-vertex totals (m at the centre) are not F32-held
+    c = np.ones(m + 1, np.uint8)
+    c[0] = 0
+    tot, vmax, live = oracle.count(g, 2, [(0, 1)], c, arith=oracle.ARITH_F64, live=True)
+    assert (tot, vmax, live) == (2.0 * m, 2.0 * m, 1.0)
+    # P3 rooted at its centre on the star, leaves alternating colours 1, 2 (4 and 3 of
+    # them): colorful = 2·4·3; the largest held entry is M_{edge}(centre,{0,1}) = 4
+    c = np.array([0] + [1, 2] * 3 + [1], np.uint8)
+    tot, vmax, live = oracle.count(g, 3, [(0, 1), (1, 2)], c, root=1, arith=oracle.ARITH_F64, live=True)
+    assert tot == 24.0 and live == 4.0 and vmax == 24.0

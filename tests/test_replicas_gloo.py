@@ -63,9 +63,11 @@ def _oracle_count_fn(case):
 def _case():
     from sg2v_inputs import erdos_renyi, TEMPLATES
     from oracle import oracle as O
+    import paper_2009_11665_b200 as sg
     e = TEMPLATES["u5-2"]
-    return {"g": erdos_renyi(200, 900, seed=3), "k": 5, "e": e,
-            "info": {"P": float(O.colorful_probability(5)), "alpha": O.alpha(5, e)}}
+    # the library's template handle (host-only): a7 runs in the C ABI (sg2v_estimate)
+    return {"g": erdos_renyi(200, 900, seed=3), "k": 5, "e": e, "info": sg.template_build(5, e),
+            "P": float(O.colorful_probability(5)), "alpha": O.alpha(5, e)}
 
 
 def _worker(rank, world, port, n_iter, q):
@@ -107,3 +109,4 @@ def test_gloo_world2_matches_single_process(n_iter):
                 assert math.isnan(est)
             else:
                 assert est == est1
+                assert math.isclose(est, sum(full1) / n_iter / (case["P"] * case["alpha"]), rel_tol=1e-12)
