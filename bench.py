@@ -158,9 +158,32 @@ def cpu_sample(args, k, edges, full_n, full_nnz, steps=1, target_s=12.0):
         O.count(g, k, edges, cols)
         out.append((time.perf_counter() - t0) * full_w / w)
     desc = (f"oracle two-stage DP (U64, OpenMP {cores} threads), 1 colouring per step of {args.template} on "
-            f"RMAT-1M-like scale {scale} (n={g.n}, nnz={g.nnz}), extrapolated x{full_w / w:.1f} to the full "
-            f"workload by the oracle's loop count sum_s nnz*C(k,p)+n*C(k,s)*C(s,a)")
+            f"RMAT-1M-like scale {scale} (n={g.n}, nnz={g.nnz}; its widest table "
+            f"{_widest_table_gb(O, k, edges, g.n):.2f} GB >> the host's L3), extrapolated x{full_w / w:.1f} to the "
+            f"full workload by the oracle's loop count sum_s nnz*C(k,p)+n*C(k,s)*C(s,a)")
     return out, desc, cores
+
+
+def _widest_table_gb(O, k, edges, n):
+    return max(math.comb(k, size) for size, _, _, _ in O.partition(k, edges, 0)) * n * 8 / 1e9
+
+
+def full_graph_oracle_record(template, scale):
+    """The oracle timed on the FULL bench graph (tools/make_golden_big.py on the GPU box's
+    host; tests/golden/big_configs.json), for cross-checking the bounded sample."""
+    if scale != 20:
+        return None
+    try:
+        cases = json.load(open(os.path.join(ROOT, "tests", "golden", "big_configs.json")))["cases"]
+    except Exception:
+        return None
+    for c in cases:
+        if c["graph"] == "rmat1m" and c["template"] == template and c.get("oracle_seconds_u64"):
+            h = c.get("host", {})
+            return {"full_graph_u64_s": c["oracle_seconds_u64"], "threads": c.get("threads"),
+                    "cpu_model": h.get("cpu_model"), "mem_total_GB": h.get("mem_total_GB"),
+                    "j": c["j"], "source": "tests/golden/big_configs.json (tools/make_golden_big.py)"}
+    return None
 
 
 # --------------------------------------------------------------------------- reference arm
@@ -177,15 +200,131 @@ def run_reference(args):
     per, desc, cores = cpu_sample(args, k, edges, n, nnz, steps=args.warmup + args.steps, target_s=6.0)
     timed = per[args.warmup:]
     v = statistics.mean(timed)
+    cb = {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": desc}
+    full = full_graph_oracle_record(args.template, args.scale)
+    if full:
+        cb["full_graph_measured"] = full
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": v * 1e3, "higher_is_better": False,
             "scaling": "weak", "vs_baseline": None, "dtype": "u64", "data": "synthetic",
             "config": {"workload": f"{args.template} on RMAT-1M-like (scale {args.scale}, n={n}, nnz={nnz})",
                        "template": args.template, "precision": "u64"},
-            "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": desc},
+            "cpu_baseline": cb,
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
+
+
+# --------------------------------------------------------------------------- roofline
+SMEM_B_PER_CLK_SM = 128      # shared-memory bandwidth per SM (B200_PROFILING.md / B300_MICROARCH.md)
+EMA_BYTES_PER_TERM = 8       # each split term reads M_a(i,I_a) and B(i,I_p) from shared memory (fp32)
+FMA_PER_CLK_SM = 128         # fp32 FMA lanes per SM
+
+
+def _peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))), "MEASURED_PEAKS.json hbm_gbs"
+    except Exception:
+        return {"hbm_gbs": 6650.0}, "of fallback (B200_PROFILING.md: 6.65 TB/s)"
+
+
+def _traffic(args):
+    """ncu DRAM bytes per launch of THIS source tree (profiles/ncu_traffic.json, stamped with
+    build.source_hash()); None when the committed capture belongs to other sources."""
+    from paper_2009_11665_b200.build import source_hash
+    try:
+        tr = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))
+    except Exception:
+        return None, "no profiles/ncu_traffic.json"
+    rec = tr.get(f"{args.template}/{args.precision}/{args.layout}/scale{args.scale}")
+    if not isinstance(rec, dict):
+        return None, "no capture for this configuration"
+    if rec.get("src_hash") != source_hash():
+        return None, f"capture {rec.get('src_hash')} is for other sources than {source_hash()} (re-run tools/traffic.sh)"
+    return rec, rec.get("source")
+
+
+def roofline(args, prof, recs, plan):
+    """Dominant kernel class: SURVEY §8(d) algorithmic bytes per launch (the plan's per-step
+    alg_bytes: useful gather + CSR + M_a + plain-width output) / the class's mean CUDA-event
+    launch time on the launching stream, against MEASURED_PEAKS hbm_gbs.  Also: the
+    implemented layout's bytes (impl), ncu DRAM traffic of this source tree, a per-step
+    table of one colouring (mean over the timed colourings), and the eMA terms/s of the
+    GENERAL steps against the shared-memory roof."""
+    peaks, psrc = _peaks()
+    peak = float(peaks.get("hbm_gbs", 6650.0))
+    sm_mhz = float(peaks.get("sm_max_mhz", 1965.0))
+    dom = max(("step", "top", "hist"), key=lambda c: prof[c]["ms"])
+    mine = [r for r in recs if r["cls"] == dom]
+    ms = sum(r["ms"] for r in mine)
+    alg = sum(r["alg_bytes"] for r in mine)
+    impl = sum(r["impl_bytes"] for r in mine)
+    nl = max(len(mine), 1)
+    achieved = alg / (ms / 1e3) / 1e9 if ms > 0 else 0.0
+    tr, tsrc = _traffic(args)
+    traffic = tr["per_class_dram_bytes_per_launch"].get(dom) if tr else None
+    rf = {"bound": "hbm", "kernel": {"step": "astep_kernel (fused SpMM + eMA, non-top steps)",
+                                     "top": "top step (fused gather + dot product)", "hist": "bucket/hist"}[dom],
+          "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+          "traffic": traffic, "traffic_source": tsrc,
+          "alg_bytes_per_launch": alg / nl, "launches": len(mine), "ms_per_launch": ms / nl,
+          "impl_bytes_per_launch": impl / nl, "impl_over_alg": impl / alg if alg else None,
+          "frac_impl": (impl / (ms / 1e3) / 1e9) / peak if ms > 0 else None,
+          "frac_dram": (traffic / (ms / nl / 1e3) / 1e9) / peak if (traffic and ms > 0) else None,
+          "peak_source": psrc,
+          "definition": "achieved = SURVEY 8(d) algorithmic bytes (plan alg_bytes: anchored useful gather "
+                        "nnz*(k-1)/k*C(k-2,p-1)*E + CSR 4*nnz + row metadata + M_a + output at plain width "
+                        "C(k-1,s-1)*E) / mean launch time (CUDA events); frac_impl uses the implemented "
+                        "layout's bytes; frac_dram uses ncu DRAM bytes of this source tree"}
+    # per-step table: records in launch order; a colouring starts at each "color" record
+    cols, cur = [], None
+    for r in recs:
+        if r["cls"] == "color":
+            cur = []
+            cols.append(cur)
+        if cur is not None:
+            cur.append(r)
+    steps_tab = []
+    if cols:
+        L = len(cols[0])
+        same = [c for c in cols if len(c) == L]
+        names = ["color", "bucket" if args.layout != "dense" else "hist"]
+        for st in plan["steps"]:
+            names.append(f"s={st['s']}={st['a']}+{st['p']}{' top' if st['top'] else ''}"
+                         f"{' self' if st.get('self') else ''}")
+        names.append("reduce")
+        for q in range(L):
+            ms_q = statistics.mean(c[q]["ms"] for c in same)
+            a_q, i_q = same[0][q]["alg_bytes"], same[0][q]["impl_bytes"]
+            steps_tab.append({"launch": names[q] if len(names) == L else same[0][q]["cls"], "ms": ms_q,
+                              "alg_GB": a_q / 1e9, "impl_GB": i_q / 1e9,
+                              "alg_frac": a_q / (ms_q / 1e3) / 1e9 / peak if ms_q > 0 else None})
+    ema = None
+    gen = [r for r in recs if r["ema_terms"] > 0]
+    if gen:
+        t_ms = sum(r["ms"] for r in gen)
+        terms = sum(r["ema_terms"] for r in gen)
+        smem_roof = 148 * SMEM_B_PER_CLK_SM * sm_mhz * 1e6 / EMA_BYTES_PER_TERM
+        fma_roof = 148 * FMA_PER_CLK_SM * sm_mhz * 1e6
+        rate = terms / (t_ms / 1e3) if t_ms > 0 else 0.0
+        ema = {"terms_per_colouring": terms / max(len(cols), 1), "ms_per_colouring": t_ms / max(len(cols), 1),
+               "terms_per_s": rate, "smem_roof_terms_per_s": smem_roof, "frac_smem": rate / smem_roof,
+               "fma_roof_per_s": fma_roof, "frac_fma": rate / fma_roof,
+               "note": "time of the GENERAL launches (gather included): a lower bound on the eMA rate"}
+    return rf, steps_tab, ema
+
+
+def _spawn_ranks(args):
+    """--gpus N without torchrun: relaunch this command under torch.distributed.run
+    (one rank per GPU, rendezvous on 127.0.0.1)."""
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
 
 
 # --------------------------------------------------------------------------- GPU arm
@@ -221,8 +360,6 @@ def run_sg2v(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    if world != args.gpus:
-        args.gpus = world
     dev = _setup_dist(world, local)
 
     import paper_2009_11665_b200 as sg
@@ -246,10 +383,22 @@ def run_sg2v(args):
     def colouring(t):  # colouring index of this rank's t-th colouring
         return rank + world * t
 
+    overflow = []  # colourings whose F32 count overflowed (EOVERFLOW), reported in the line
+
+    def count(GG, n_iter, off, stride=1, wsp=ws):
+        try:
+            return sg.count(GG, T, n_iter=n_iter, seed=args.seed, iter_offset=off, iter_stride=stride,
+                            precision=args.precision, workspace=wsp, layout=args.layout)
+        except sg.Sg2vError as ex:
+            if ex.code != sg.sg2v.EOVERFLOW:
+                raise
+            overflow.append(off)
+            return sg.count(GG, T, n_iter=n_iter, seed=args.seed, iter_offset=off, iter_stride=stride,
+                            precision=args.precision, workspace=wsp, layout=args.layout, allow_overflow=True)
+
     # warm-up (untimed)
     for t in range(args.warmup):
-        sg.count(G, T, n_iter=1, seed=args.seed, iter_offset=colouring(t), precision=args.precision,
-                 workspace=ws, allow_overflow=True, layout=args.layout)
+        count(G, 1, colouring(t))
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
@@ -261,8 +410,7 @@ def run_sg2v(args):
     with Clocks(dev) as clk:
         torch.cuda.synchronize()
         ev0.record(stream)
-        est, c = sg.count(G, T, n_iter=args.steps, seed=args.seed, iter_offset=colouring(args.warmup),
-                          iter_stride=world, precision=args.precision, workspace=ws, allow_overflow=True, layout=args.layout)
+        est, c = count(G, args.steps, colouring(args.warmup), world)
         for t in range(args.steps):
             counts[rank + world * t] = float(c[t])
         if world > 1:
@@ -270,6 +418,7 @@ def run_sg2v(args):
         ev1.record(stream)
         torch.cuda.synchronize()
     prof = sg.profile_read()
+    launches_rec = sg.profile_read_launches()
     sg.profile_enable(False)
     dev_s = ev0.elapsed_time(ev1) / 1e3
     t_max = torch.tensor([dev_s], dtype=torch.float64, device=_dist_device())
@@ -279,8 +428,12 @@ def run_sg2v(args):
     value = float(t_max.item()) / total
 
     # ---- e2e: the public API from pinned HOST buffers, copies inside the timed region ----
+    # (the workspace is requested inside the timed region too, as a user's call does;
+    # torch's caching allocator hands back the same block after the first step)
     e2e_steps = args.e2e_steps if args.e2e_steps is not None else args.steps
     del G
+    ws_bytes = ws.nbytes
+    del ws
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
@@ -288,9 +441,10 @@ def run_sg2v(args):
     e0.record(stream)
     for t in range(e2e_steps):
         Ge = sg.graph_load_csr(g.n, ro_h.numpy(), ci_h.numpy())
-        sg.count(Ge, T, n_iter=1, seed=args.seed, iter_offset=colouring(args.warmup + args.steps + t),
-                 precision=args.precision, workspace=ws, allow_overflow=True, layout=args.layout)  # includes D2H of the count
+        wse = sg.Workspace(ws_bytes)
+        count(Ge, 1, colouring(args.warmup + args.steps + t), wsp=wse)  # includes D2H of the count
         Ge.free()
+        del wse
     e1.record(stream)
     torch.cuda.synchronize()
     e_max = torch.tensor([e0.elapsed_time(e1) / 1e3], dtype=torch.float64, device=_dist_device())
@@ -305,24 +459,7 @@ def run_sg2v(args):
         return 0
 
     # ---- roofline of the dominant kernel class (live CUDA events on the launching stream) ----
-    dom = max(("step", "top", "hist"), key=lambda c: prof[c]["ms"])
-    peaks = {}
-    try:
-        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
-    except Exception:
-        pass
-    peak = float(peaks.get("hbm_gbs", 6650.0))
-    achieved = prof[dom]["bytes"] / (prof[dom]["ms"] / 1e3) / 1e9 if prof[dom]["ms"] > 0 else 0.0
-    traffic = None
-    tr_path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
-    if os.path.exists(tr_path):
-        try:
-            tr = json.load(open(tr_path))
-            key = f"{args.template}/{args.precision}/{args.layout}/scale{args.scale}"
-            if key in tr:
-                traffic = tr[key]
-        except Exception:
-            traffic = None
+    rf, steps_tab, ema = roofline(args, prof, launches_rec, plan)
     launches = prof["color"]["launches"] + prof["hist"]["launches"] + prof["step"]["launches"] + \
         prof["top"]["launches"] + 2 * prof["reduce"]["launches"]
     clocks = clk.summary()
@@ -338,19 +475,23 @@ def run_sg2v(args):
                    "l2": "inputs larger than L2 (CSR %.2f GB + count tables %.1f GB >> 126 MB); no flush"
                          % (g.nbytes() / 1e9, plan["tables_bytes"] / 1e9)},
         "estimate": est, "colorful_first": float(c[0]),
+        "status": "EOVERFLOW" if overflow else "OK", "overflowed_colourings": len(overflow),
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(g.nbytes()),
                 "d2h_bytes_per_step": 8},
         "gpu_launches": int(launches),
         "kernel_ms_per_step": {kk: v["ms"] / args.steps for kk, v in prof.items()},
-        "roofline": {"bound": "hbm", "kernel": f"{dom} (fused SpMM+eMA, all launches)" if dom == "step" else dom,
-                     "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                     "traffic": traffic, "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback",
-                     "bytes_per_step": prof[dom]["bytes"] / args.steps},
+        "roofline": rf,
+        "steps_per_colouring": steps_tab,
         "clocks": clocks,
     }
+    if ema:
+        line["ema"] = ema
     if world == 1 and not args.no_cpu_baseline:
         per, desc, cores = cpu_sample(args, k, edges, g.n, g.nnz, steps=1)
         line["cpu_baseline"] = {"value": per[0], "unit": UNIT, "cores": cores, "kind": "oracle", "sample": desc}
+        full = full_graph_oracle_record(args.template, args.scale)
+        if full:
+            line["cpu_baseline"]["full_graph_measured"] = full
     print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()
@@ -367,7 +508,6 @@ def run_vertex(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    args.gpus = world
     dev = _setup_dist(world, local)
     import paper_2009_11665_b200 as sg
     from paper_2009_11665_b200.build import build
@@ -458,6 +598,12 @@ def run_vertex(args):
 
 def main():
     args = _args()
+    world = os.environ.get("WORLD_SIZE")
+    if args.gpus > 1 and world is None:
+        return _spawn_ranks(args)
+    if world is not None and int(world) != args.gpus:
+        print(json.dumps({"error": f"--gpus {args.gpus} but WORLD_SIZE={world}"}), flush=True)
+        return 2
     if args.impl == "reference":
         return run_reference(args)
     if args.mode == "vertex":

@@ -258,6 +258,14 @@ sg2v_status sg2v_plan_describe_n(int64_t n, int64_t nnz, const sg2v_template *t,
  */
 sg2v_status sg2v_profile_enable(int32_t on);
 sg2v_status sg2v_profile_read(int64_t launches[5], double ms[5], double bytes[5]);
+/* Per-launch records of the same profile, in launch order (q < min(cap, *n_out)):
+ * class (0..4 as above), CUDA-event ms on the launching stream, the launch's
+ * algorithmic bytes (the method's useful gather + CSR + M_a + output at
+ * plain width — independent of the table layout the planner chose), its impl bytes
+ * (the implemented layout: plain-width gathers of plain sources, projected-copy
+ * writes) and its eMA split terms (GENERAL steps).  *n_out = number of records. */
+sg2v_status sg2v_profile_read_launches(int64_t cap, int32_t *cls, double *ms, double *alg_bytes,
+                                       double *impl_bytes, double *ema_terms, int64_t *n_out);
 
 const char *sg2v_last_error(void);
 const char *sg2v_version(void);

@@ -258,6 +258,154 @@ __device__ __forceinline__ void gather_row(const AStepArgs &A, int64_t i, int ci
     }
 }
 
+// ---- stage 2 for one slot (V rows of a group): eMA over the universe [k-1] and the
+// stores, or the top dot product + per-vertex value (shared by the register-gather and
+// the bulk-staged kernels) ----
+template <typename T, typename RT, int GT, int V>
+__device__ __forceinline__ void ema_stage(const AStepArgs &A, T *sBase, const int64_t *iv, const bool *actv, int t,
+                                          int g, RT *red, bool &bad) {
+    constexpr int VN = Vec<T>::N;
+    RT racc = 0;
+    if (!A.top && A.comb == COMB_ACTIVE_LEAF) {
+        // M_s(i,·) = B(i,·): |T_s| - 1 = |T_p| and the colour sets coincide
+#pragma unroll
+        for (int v = 0; v < V; ++v)
+            if (actv[v]) {
+                const T *sB = sBase + (size_t)v * A.smem_group;
+                if (A.ms) {  // plain table
+                    T *out = reinterpret_cast<T *>(A.ms) + (size_t)iv[v] * A.lds;
+                    for (int64_t q = t; q < A.lds / VN; q += GT) {
+                        const uint4 w = reinterpret_cast<const uint4 *>(sB)[q];
+                        bad |= nonfinite4<T>(w);
+                        __stcs(reinterpret_cast<uint4 *>(out) + q, w);
+                    }
+                }
+                if (A.msx) {
+                    // projected: segment y' position u <- B(i, omap[y'][u]) (16-B stores)
+                    T *out = reinterpret_cast<T *>(A.msx) + (size_t)iv[v] * A.ldsx;
+                    for (int64_t q = t; q < A.ldsx / VN; q += GT) {
+                        uint4 w;
+#pragma unroll
+                        for (int el = 0; el < VN; ++el) {
+                            const int32_t c = __ldg(A.omap + q * VN + el);
+                            vset<T>(w, el, c >= 0 ? sB[c] : (T)0);
+                        }
+                        bad |= nonfinite4<T>(w);
+                        __stcs(reinterpret_cast<uint4 *>(out) + q, w);
+                    }
+                }
+            }
+    } else if (!A.top) {
+        // split table term-major: entry (w, o) at w*cs + o, so the lanes (consecutive
+        // outputs o) read consecutive words; each entry serves the group's V rows.
+        // With few outputs (cs < GT) tpo consecutive lanes share an output.
+        const int tpo = A.tpo, cs = (int)A.cs, nt = (int)A.nterms, lds = (int)A.ocols;
+        const int l = t % tpo;
+        for (int ob = 0; ob < lds; ob += GT / tpo) {
+            const int o = ob + t / tpo;
+            T acc[V];
+#pragma unroll
+            for (int v = 0; v < V; ++v) acc[v] = 0;
+            if (o < cs) {
+                if (V > 1 && A.packed && A.stage_a) {
+                    // interleaved rows: entry e of the V rows is sBase[e*V .. e*V+V)
+                    const uint32_t *p = reinterpret_cast<const uint32_t *>(A.idx) + o;
+                    constexpr int NV = (V * (int)sizeof(T)) / 16;  // 16-B vectors per entry
+#pragma unroll 16
+                    for (int w = l; w < nt; w += tpo) {
+                        const uint32_t q = __ldg(p + w * cs);
+                        const uint32_t ia = (q & 0xffffu) + (uint32_t)A.aoff, ib = q >> 16;
+                        const uint4 *pa = reinterpret_cast<const uint4 *>(sBase + (size_t)ia * V);
+                        const uint4 *pb = reinterpret_cast<const uint4 *>(sBase + (size_t)ib * V);
+#pragma unroll
+                        for (int z = 0; z < NV; ++z) {
+                            const uint4 va = pa[z], vb = pb[z];
+#pragma unroll
+                            for (int e = 0; e < 16 / (int)sizeof(T); ++e)
+                                acc[z * (16 / (int)sizeof(T)) + e] += vget<T>(va, e) * vget<T>(vb, e);
+                        }
+                    }
+                } else if (A.packed && A.stage_a) {
+                    const uint32_t *p = reinterpret_cast<const uint32_t *>(A.idx) + o;
+#pragma unroll 4
+                    for (int w = l; w < nt; w += tpo) {
+                        const uint32_t q = __ldg(p + w * cs);
+                        const uint32_t ia = q & 0xffffu, ib = q >> 16;
+#pragma unroll
+                        for (int v = 0; v < V; ++v) {
+                            const T *sB = sBase + (size_t)v * A.smem_group;
+                            acc[v] += sB[A.aoff + ia] * sB[ib];
+                        }
+                    }
+                } else {
+                    for (int w = l; w < nt; w += tpo) {
+                        int32_t ia, ib;
+                        if (A.packed) {
+                            const uint32_t q = __ldg(reinterpret_cast<const uint32_t *>(A.idx) + o + (size_t)w * cs);
+                            ia = (int32_t)(q & 0xffffu);
+                            ib = (int32_t)(q >> 16);
+                        } else {
+                            const int2 q = __ldg(reinterpret_cast<const int2 *>(A.idx) + o + (size_t)w * cs);
+                            ia = q.x;
+                            ib = q.y;
+                        }
+#pragma unroll
+                        for (int v = 0; v < V; ++v) {
+                            const T *sB = V > 1 ? sBase + v : sBase + (size_t)v * A.smem_group;
+                            const int64_t sv = V > 1 ? V : 1;
+                            const T av = A.stage_a ? sB[(A.aoff + ia) * sv]
+                                                   : __ldg(reinterpret_cast<const T *>(A.ma) + (size_t)iv[v] * A.lda + ia);
+                            acc[v] += av * sB[ib * sv];
+                        }
+                    }
+                }
+            }
+#pragma unroll
+            for (int v = 0; v < V; ++v) {
+                if (tpo > 1) {  // tpo <= 32 and GT >= 32: whole warps, uniform trip count
+#pragma unroll
+                    for (int off = 16; off > 0; off >>= 1)
+                        if (off < tpo) acc[v] += __shfl_xor_sync(0xffffffffu, acc[v], off);
+                }
+                if (actv[v] && l == 0 && o < lds) {
+                    bad |= nonfinite<T>(acc[v]);
+                    if (A.ms) __stcs(reinterpret_cast<T *>(A.ms) + (size_t)iv[v] * A.lds + o, acc[v]);
+                    if (A.msx && o < cs) {  // projected: every segment y' ∌ o
+                        T *orow = reinterpret_cast<T *>(A.msx) + (size_t)iv[v] * A.ldsx;
+#pragma unroll 1
+                        for (int y = 0; y < A.k - 1; ++y) {
+                            const int32_t pos = __ldg(A.omap + (size_t)o * (A.k - 1) + y);
+                            if (pos >= 0) __stcs(orow + (size_t)y * A.ldseg_out + pos, acc[v]);
+                        }
+                    }
+                }
+            }
+        }
+    } else if (actv[0]) {
+        // top (V == 1): colorful_i = Σ_{I_a} M_a(i,I_a)·B(i,[k-1]∖I_a)
+        const T *sB = sBase;
+        const T *ga = reinterpret_cast<const T *>(A.ma) + (size_t)iv[0] * A.lda;
+        for (int64_t w = t; w < A.nterms; w += GT) {
+            int32_t ia, ib;
+            if (A.packed) {
+                const uint32_t q = __ldg(reinterpret_cast<const uint32_t *>(A.idx) + w);
+                ia = (int32_t)(q & 0xffffu);
+                ib = (int32_t)(q >> 16);
+            } else {
+                const int2 q = __ldg(reinterpret_cast<const int2 *>(A.idx) + w);
+                ia = q.x;
+                ib = q.y;
+            }
+            const T av = A.stage_a ? sB[A.aoff + ia] : __ldg(ga + ia);
+            racc += (RT)av * (RT)sB[ib];
+        }
+    }
+    if (A.top) {
+        RT s = group_reduce<RT, GT>(racc, g, red);
+        if (actv[0] && t == 0) reinterpret_cast<RT *>(A.rowval)[iv[0]] = s;
+    }
+}
+
 // GT threads per row group; R 16-B vectors per thread per pass; U neighbours in
 // flight; V rows per group per slot (V > 1 only for GENERAL non-top steps: each
 // split-table entry is loaded once and applied to V rows).
@@ -363,147 +511,157 @@ __global__ void __launch_bounds__(256, AStepMinBlocks<U, V, MODE>::value) astep_
             }
         }
         group_sync<GT>(g);
-        // ---- stage 2: eMA over the universe [k-1] ------------------------------
-        RT racc = 0;
-        if (!A.top && A.comb == COMB_ACTIVE_LEAF) {
-            // M_s(i,·) = B(i,·): |T_s| - 1 = |T_p| and the colour sets coincide
-#pragma unroll
-            for (int v = 0; v < V; ++v)
-                if (actv[v]) {
-                    const T *sB = sBase + (size_t)v * A.smem_group;
-                    if (A.ms) {  // plain table
-                        T *out = reinterpret_cast<T *>(A.ms) + (size_t)iv[v] * A.lds;
-                        for (int64_t q = t; q < A.lds / VN; q += GT) {
-                            const uint4 w = reinterpret_cast<const uint4 *>(sB)[q];
-                            bad |= nonfinite4<T>(w);
-                            __stcs(reinterpret_cast<uint4 *>(out) + q, w);
-                        }
-                    }
-                    if (A.msx) {
-                        // projected: segment y' position u <- B(i, omap[y'][u]) (16-B stores)
-                        T *out = reinterpret_cast<T *>(A.msx) + (size_t)iv[v] * A.ldsx;
-                        for (int64_t q = t; q < A.ldsx / VN; q += GT) {
-                            uint4 w;
-#pragma unroll
-                            for (int el = 0; el < VN; ++el) {
-                                const int32_t c = __ldg(A.omap + q * VN + el);
-                                vset<T>(w, el, c >= 0 ? sB[c] : (T)0);
-                            }
-                            bad |= nonfinite4<T>(w);
-                            __stcs(reinterpret_cast<uint4 *>(out) + q, w);
-                        }
-                    }
-                }
-        } else if (!A.top) {
-            // split table term-major: entry (w, o) at w*cs + o, so the lanes (consecutive
-            // outputs o) read consecutive words; each entry serves the group's V rows.
-            // With few outputs (cs < GT) tpo consecutive lanes share an output.
-            const int tpo = A.tpo, cs = (int)A.cs, nt = (int)A.nterms, lds = (int)A.ocols;
-            const int l = t % tpo;
-            for (int ob = 0; ob < lds; ob += GT / tpo) {
-                const int o = ob + t / tpo;
-                T acc[V];
-#pragma unroll
-                for (int v = 0; v < V; ++v) acc[v] = 0;
-                if (o < cs) {
-                    if (V > 1 && A.packed && A.stage_a) {
-                        // interleaved rows: entry e of the V rows is sBase[e*V .. e*V+V)
-                        const uint32_t *p = reinterpret_cast<const uint32_t *>(A.idx) + o;
-                        constexpr int NV = (V * (int)sizeof(T)) / 16;  // 16-B vectors per entry
-#pragma unroll 16
-                        for (int w = l; w < nt; w += tpo) {
-                            const uint32_t q = __ldg(p + w * cs);
-                            const uint32_t ia = (q & 0xffffu) + (uint32_t)A.aoff, ib = q >> 16;
-                            const uint4 *pa = reinterpret_cast<const uint4 *>(sBase + (size_t)ia * V);
-                            const uint4 *pb = reinterpret_cast<const uint4 *>(sBase + (size_t)ib * V);
-#pragma unroll
-                            for (int z = 0; z < NV; ++z) {
-                                const uint4 va = pa[z], vb = pb[z];
-#pragma unroll
-                                for (int e = 0; e < 16 / (int)sizeof(T); ++e)
-                                    acc[z * (16 / (int)sizeof(T)) + e] += vget<T>(va, e) * vget<T>(vb, e);
-                            }
-                        }
-                    } else if (A.packed && A.stage_a) {
-                        const uint32_t *p = reinterpret_cast<const uint32_t *>(A.idx) + o;
-#pragma unroll 4
-                        for (int w = l; w < nt; w += tpo) {
-                            const uint32_t q = __ldg(p + w * cs);
-                            const uint32_t ia = q & 0xffffu, ib = q >> 16;
-#pragma unroll
-                            for (int v = 0; v < V; ++v) {
-                                const T *sB = sBase + (size_t)v * A.smem_group;
-                                acc[v] += sB[A.aoff + ia] * sB[ib];
-                            }
-                        }
-                    } else {
-                        for (int w = l; w < nt; w += tpo) {
-                            int32_t ia, ib;
-                            if (A.packed) {
-                                const uint32_t q = __ldg(reinterpret_cast<const uint32_t *>(A.idx) + o + (size_t)w * cs);
-                                ia = (int32_t)(q & 0xffffu);
-                                ib = (int32_t)(q >> 16);
-                            } else {
-                                const int2 q = __ldg(reinterpret_cast<const int2 *>(A.idx) + o + (size_t)w * cs);
-                                ia = q.x;
-                                ib = q.y;
-                            }
-#pragma unroll
-                            for (int v = 0; v < V; ++v) {
-                                const T *sB = V > 1 ? sBase + v : sBase + (size_t)v * A.smem_group;
-                                const int64_t sv = V > 1 ? V : 1;
-                                const T av = A.stage_a ? sB[(A.aoff + ia) * sv]
-                                                       : __ldg(reinterpret_cast<const T *>(A.ma) + (size_t)iv[v] * A.lda + ia);
-                                acc[v] += av * sB[ib * sv];
-                            }
-                        }
-                    }
-                }
-#pragma unroll
-                for (int v = 0; v < V; ++v) {
-                    if (tpo > 1) {  // tpo <= 32 and GT >= 32: whole warps, uniform trip count
-#pragma unroll
-                        for (int off = 16; off > 0; off >>= 1)
-                            if (off < tpo) acc[v] += __shfl_xor_sync(0xffffffffu, acc[v], off);
-                    }
-                    if (actv[v] && l == 0 && o < lds) {
-                        bad |= nonfinite<T>(acc[v]);
-                        if (A.ms) __stcs(reinterpret_cast<T *>(A.ms) + (size_t)iv[v] * A.lds + o, acc[v]);
-                        if (A.msx && o < cs) {  // projected: every segment y' ∌ o
-                            T *orow = reinterpret_cast<T *>(A.msx) + (size_t)iv[v] * A.ldsx;
-#pragma unroll 1
-                            for (int y = 0; y < A.k - 1; ++y) {
-                                const int32_t pos = __ldg(A.omap + (size_t)o * (A.k - 1) + y);
-                                if (pos >= 0) __stcs(orow + (size_t)y * A.ldseg_out + pos, acc[v]);
-                            }
-                        }
-                    }
-                }
-            }
-        } else if (actv[0]) {
-            // top (V == 1): colorful_i = Σ_{I_a} M_a(i,I_a)·B(i,[k-1]∖I_a)
-            const T *sB = sBase;
-            const T *ga = reinterpret_cast<const T *>(A.ma) + (size_t)iv[0] * A.lda;
-            for (int64_t w = t; w < A.nterms; w += GT) {
-                int32_t ia, ib;
-                if (A.packed) {
-                    const uint32_t q = __ldg(reinterpret_cast<const uint32_t *>(A.idx) + w);
-                    ia = (int32_t)(q & 0xffffu);
-                    ib = (int32_t)(q >> 16);
-                } else {
-                    const int2 q = __ldg(reinterpret_cast<const int2 *>(A.idx) + w);
-                    ia = q.x;
-                    ib = q.y;
-                }
-                const T av = A.stage_a ? sB[A.aoff + ia] : __ldg(ga + ia);
-                racc += (RT)av * (RT)sB[ib];
-            }
-        }
-        if (A.top) {
-            RT s = group_reduce<RT, GT>(racc, g, red);
-            if (actv[0] && t == 0) reinterpret_cast<RT *>(A.rowval)[iv[0]] = s;
-        }
+        ema_stage<T, RT, GT, V>(A, sBase, iv, actv, t, g, red, bad);
         group_sync<GT>(g);
+    }
+    if (bad) atomicOr(A.ovf, 1);
+}
+
+// ---------------------------------------------------------------------------
+// bulk-staged fused step (wide rows): the gather of stage 1 is fed by the TMA engine.
+// One producer warp walks the neighbour list of the CTA's rows in colour-bucket order
+// (the row's own colour skipped) and issues one cp.async.bulk per neighbour — its whole
+// anchored row, or for an exclusion-projected source its segment c(i) — into a ring of
+// S shared-memory stages (full/empty mbarriers); the 256 consumer threads add each
+// staged row into per-colour register sums R_x (lane t owns 16-B vectors t, t+256, ...),
+// push R_x into B(i,·) through the [x][c(i)] map at every colour boundary (one named
+// barrier per colour, as in gather_row), then run the same eMA / top epilogue
+// (ema_stage).  Loads need no registers and run up to S rows ahead across colour and
+// row boundaries, so memory-level parallelism no longer depends on the consumers'
+// register budget, and a consumer spends ~6 instructions per 16-B vector instead of
+// the register-gather's index/policy/address work per neighbour.
+// ---------------------------------------------------------------------------
+static constexpr int kBulkConsumers = 256;
+static constexpr int kBulkThreads = kBulkConsumers + 32;
+
+template <typename T, typename RT, int R>
+__global__ void __launch_bounds__(kBulkThreads, 3) astep_bulk_kernel(AStepArgs A, int S, uint32_t stage_bytes) {
+    constexpr int VN = Vec<T>::N;
+    constexpr int32_t kIdMask = (1 << kClassShift) - 1;
+    extern __shared__ __align__(128) unsigned char smem[];
+    __shared__ RT red[8];
+    uint64_t *full = reinterpret_cast<uint64_t *>(smem);
+    uint64_t *empty = full + S;
+    T *sB = reinterpret_cast<T *>(smem + ((2 * S * 8 + 127) / 128) * 128);
+    unsigned char *stages = reinterpret_cast<unsigned char *>(sB) + ((A.smem_group * sizeof(T) + 127) / 128) * 128;
+    const int tid = threadIdx.x;
+    const int k = A.k;
+    const int64_t nvec_p = (A.ldseg_p > 0 ? A.ldseg_p : A.ldp) / VN;
+    const uint32_t seg_bytes = (uint32_t)(nvec_p * 16);
+    const size_t row_bytes = (size_t)A.ldp * sizeof(T);
+    if (tid == 0) {
+        for (int q = 0; q < S; ++q) {
+            mbar_init(full + q, 1);
+            mbar_init(empty + q, kBulkConsumers / 32);
+        }
+        fence_mbar_init();
+    }
+    __syncthreads();
+    const int64_t n = A.n;
+    if (tid >= kBulkConsumers) {
+        // ---------------- producer warp ----------------
+        const int lane = tid & 31;
+        const uint64_t pol_last = policy_evict_last(), pol_first = A.hint ? policy_evict_first() : policy_evict_normal();
+        int slot = 0;
+        uint32_t ph = 0;
+        for (int64_t r = blockIdx.x; r < n; r += gridDim.x) {
+            const int64_t i = A.order[r];
+            const int ci = A.colors[i];
+            const int64_t e0 = A.rowptr[i];
+            // lane x holds this row's count of colour x
+            const int hx = lane < k ? __ldg(A.hcnt + (size_t)i * A.kp + lane) : 0;
+            int x = -1, left = 0;     // current colour bucket and its remaining neighbours
+            int64_t e = e0;
+            for (;;) {
+                // advance to the next non-empty bucket of a colour != ci (warp-uniform)
+                while (left == 0) {
+                    ++x;
+                    if (x >= k) break;
+                    const int c = __shfl_sync(0xffffffffu, hx, x);
+                    if (x == ci) { e += c; continue; }
+                    left = c;
+                }
+                if (x >= k) break;
+                const int take = left < 32 ? left : 32;
+                const int32_t b = lane < take ? __ldg(A.bcol + e + lane) : 0;
+                const int rr = ci - (ci > x ? 1 : 0);
+                const int64_t sbase = A.ldseg_p > 0 ? (int64_t)rr * A.ldseg_p * (int64_t)sizeof(T) : 0;
+                for (int q = 0; q < take; ++q) {
+                    const int32_t bj = __shfl_sync(0xffffffffu, b, q);
+                    if (lane == 0) {
+                        const int32_t j = A.tagged ? (bj & kIdMask) : bj;
+                        const uint64_t pol = (A.tagged && (bj >> kClassShift) < A.hot_log2) ? pol_last : pol_first;
+                        mbar_wait(empty + slot, ph ^ 1);
+                        mbar_arrive_expect_tx(full + slot, seg_bytes);
+                        bulk_g2s(stages + (size_t)slot * stage_bytes, A.mp + (size_t)j * row_bytes + sbase, seg_bytes,
+                                 full + slot, pol);
+                    }
+                    if (++slot == S) { slot = 0; ph ^= 1; }
+                }
+                e += take;
+                left -= take;
+            }
+        }
+        return;
+    }
+    // ---------------- consumers (256 threads = one row group) ----------------
+    const int t = tid;
+    const int lane = tid & 31;
+    bool bad = false;
+    int slot = 0;
+    uint32_t ph = 0;
+    for (int64_t r = blockIdx.x; r < n; r += gridDim.x) {
+        int64_t iv[1];
+        bool actv[1] = {true};
+        const int64_t i = A.order[r];
+        iv[0] = i;
+        const int ci = A.colors[i];
+        for (int64_t q = t; q < A.ldb / VN; q += kBulkConsumers) reinterpret_cast<uint4 *>(sB)[q] = make_uint4(0, 0, 0, 0);
+        if (A.comb == COMB_GENERAL && A.stage_a && A.aoff != 0) {
+            const char *a = A.ma + (size_t)i * A.lda * sizeof(T);
+            for (int64_t q = t; q < A.lda / VN; q += kBulkConsumers)
+                reinterpret_cast<uint4 *>(sB + A.ldb)[q] = ldg16(a + q * 16);
+        }
+        group_sync<kBulkConsumers>(0);
+        const int32_t *h = A.hcnt + (size_t)i * A.kp;
+        for (int x = 0; x < k; ++x) {
+            const int cnt = __ldg(h + x);
+            if (x == ci || cnt == 0) continue;
+            uint4 acc[R];
+#pragma unroll
+            for (int q = 0; q < R; ++q) acc[q] = make_uint4(0, 0, 0, 0);
+            for (int c = 0; c < cnt; ++c) {
+                mbar_wait(full + slot, ph);
+                const unsigned char *st = stages + (size_t)slot * stage_bytes;
+#pragma unroll
+                for (int q = 0; q < R; ++q) {
+                    const int v = t + q * kBulkConsumers;
+                    if (v < nvec_p) Vec<T>::add(acc[q], lds16(st + (size_t)v * 16));
+                }
+                __syncwarp();
+                if (lane == 0) mbar_arrive(empty + slot);
+                if (++slot == S) { slot = 0; ph ^= 1; }
+            }
+            // push R_x into B: distinct targets within one colour
+            const int32_t *mp = A.pmap + ((size_t)x * k + ci) * A.cp_map + A.u0;
+#pragma unroll
+            for (int q = 0; q < R; ++q) {
+                const int64_t v = t + q * kBulkConsumers;
+                if (v < nvec_p) {
+#pragma unroll
+                    for (int el = 0; el < VN; ++el) {
+                        const int64_t u = v * VN + el;
+                        if (u < A.cp) {
+                            const int32_t tt = __ldg(mp + u);
+                            if (tt >= 0) sB[tt] += vget<T>(acc[q], el);
+                        }
+                    }
+                }
+            }
+            group_sync<kBulkConsumers>(0);  // colours x and x' may push to the same T
+        }
+        ema_stage<T, RT, kBulkConsumers, 1>(A, sB, iv, actv, t, 0, red, bad);
+        group_sync<kBulkConsumers>(0);
     }
     if (bad) atomicOr(A.ovf, 1);
 }
@@ -582,6 +740,34 @@ static int launch_astep_t(const AStepArgs &A, void *stream) {
     return (int)cudaGetLastError();
 }
 
+// Bulk-staged launch (astep_bulk_kernel): R 16-B vectors per consumer lane, S stages
+// sized for ~48 KB of bulk copies in flight per CTA (3 CTAs per SM).
+template <typename T, typename RT, int R>
+static int launch_astep_bulk_t(const AStepArgs &A, void *stream) {
+    constexpr int VN = Vec<T>::N;
+    const int64_t nvec_p = (A.ldseg_p > 0 ? A.ldseg_p : A.ldp) / VN;
+    const uint32_t stage_bytes = (uint32_t)(((nvec_p * 16) + 127) / 128 * 128);
+    static int want_kb = -1;  // SG2V_BULK_KB (experiments): bulk bytes in flight per CTA
+    if (want_kb < 0) { const char *e = getenv("SG2V_BULK_KB"); want_kb = e ? atoi(e) : 48; }
+    int S = (int)std::max<int64_t>(3, std::min<int64_t>(16, ((int64_t)want_kb * 1024) / stage_bytes));
+    auto smem_of = [&](int s) {
+        return (size_t)((2 * s * 8 + 127) / 128 * 128) + (size_t)((A.smem_group * sizeof(T) + 127) / 128 * 128) +
+               (size_t)s * stage_bytes;
+    };
+    while (S > 3 && smem_of(S) > 220 * 1024) --S;
+    const size_t smem = smem_of(S);
+    if (smem > 227 * 1024) return -1;
+    auto kern = astep_bulk_kernel<T, RT, R>;
+    if (cudaError_t e = ensure_dyn_smem((const void *)kern, smem)) return (int)e;
+    int occ = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kBulkThreads, smem);
+    if (occ < 1) occ = 1;
+    int64_t blocks = std::min<int64_t>(A.n, (int64_t)occ * num_sms());
+    if (blocks < 1) blocks = 1;
+    kern<<<(unsigned)blocks, kBulkThreads, smem, (cudaStream_t)stream>>>(A, S, stage_bytes);
+    return (int)cudaGetLastError();
+}
+
 // Row-group configuration: narrow rows give every vector of the passive row its own
 // lane (R = 1) and keep U = 8 neighbours in flight; rows wider than 256 vectors use
 // the whole CTA, one vector per lane per pass, also U = 8 (64 registers, 4 CTAs per
@@ -631,6 +817,21 @@ static int launch_astep_cfg(const AStepArgs &A0, void *stream) {
     const bool multi = A.comb == COMB_GENERAL && !A.top && A.nterms >= 8 && gt >= 32 && tune != 5 &&
                        (A.terms_per_byte >= vtpb || tune == 9) &&
                        (size_t)(256 / gt) * 4 * A.smem_group * sizeof(T) <= 200 * 1024;
+    // wide gather rows without V-row batching: bulk-staged loads (SG2V_BULK=0 disables,
+    // SG2V_BULK_MIN sets the minimum row width in 16-B vectors)
+    static int bulk = -1, bulk_min = -1;
+    if (bulk < 0) {
+        const char *e = getenv("SG2V_BULK");
+        bulk = e ? atoi(e) : 1;
+        const char *m = getenv("SG2V_BULK_MIN");
+        bulk_min = m ? atoi(m) : 64;
+    }
+    if (MODE == 0 && bulk && !multi && !A.src_hist && A.pmap != nullptr && nvec >= bulk_min && nvec <= 2048) {
+        if (nvec <= 256) return launch_astep_bulk_t<T, RT, 1>(A, stream);
+        if (nvec <= 512) return launch_astep_bulk_t<T, RT, 2>(A, stream);
+        if (nvec <= 1024) return launch_astep_bulk_t<T, RT, 4>(A, stream);
+        return launch_astep_bulk_t<T, RT, 8>(A, stream);
+    }
     if constexpr (MODE != 0) {
         if constexpr (MODE == 2) {
             if (multi) {
@@ -695,7 +896,7 @@ int launch_astep_vp(const Graph &g, const Plan &pl, const Step &st, const uint8_
             atop_leaf_kernel<u64, u64><<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(
                 g.n, pl.k, (int)pl.kp, g.d_rowptr, g.d_col, colors, hcnt, (const u64 *)src, st.ldp, srch, idx,
                 (u64 *)rowval);
-        prof_end(3, st.alg_bytes, stream);
+        prof_end(3, st.alg_bytes, stream, st.impl_bytes, 0.0);
         return (int)cudaGetLastError();
     }
     AStepArgs A;
@@ -721,7 +922,7 @@ int launch_astep_vp(const Graph &g, const Plan &pl, const Step &st, const uint8_
     A.ldseg_out = st.proj_out ? st.ldseg_out : 0;
     A.msx = (!st.top && st.proj_out && st.buf_outx >= 0) ? tables + pl.bufs[st.buf_outx].offset : nullptr;
     A.ldsx = st.ldsx;
-    A.terms_per_byte = st.alg_bytes > 0 ? st.ema_terms / st.alg_bytes : 1.0;
+    A.terms_per_byte = st.impl_bytes > 0 ? st.ema_terms / st.impl_bytes : 1.0;
     A.omap = st.omap_off >= 0 ? pl.d_index + st.omap_off : nullptr;
     A.ocols = st.top ? 1 : (st.cs + (16 / pl.elem) - 1) / (16 / pl.elem) * (16 / pl.elem);
     A.ldb = st.ldb;
@@ -795,8 +996,9 @@ int launch_astep_vp(const Graph &g, const Plan &pl, const Step &st, const uint8_
         rc = md == 1 ? launch_astep_cfg<u64, u64, 1>(A, stream)
                      : md == 2 ? launch_astep_cfg<u64, u64, 2>(A, stream) : launch_astep_cfg<u64, u64, 0>(A, stream);
     // algorithmic bytes of a column tile: its share of the step's gather
-    prof_end(cls, !vp ? st.alg_bytes : (vp->mode == 1 ? st.alg_bytes * (double)vp->cnt / (double)std::max<int64_t>(st.cp, 1) : 0.0),
-             stream);
+    const double tile_frac = !vp ? 1.0 : (vp->mode == 1 ? (double)vp->cnt / (double)std::max<int64_t>(st.cp, 1) : 0.0);
+    prof_end(cls, st.alg_bytes * tile_frac, stream, st.impl_bytes * tile_frac,
+             !vp || vp->mode == 2 ? st.ema_terms : 0.0);
     return rc;
 }
 

@@ -84,7 +84,7 @@ Template::~Template() {
 struct ProfRec {
     int cls;
     cudaEvent_t a, b;
-    double bytes;
+    double bytes, impl, terms;
 };
 static std::mutex g_prof_mu;
 static bool g_prof_on = false;
@@ -110,12 +110,12 @@ void prof_begin(int, void *stream) {
     cudaEventRecord(g_pending, (cudaStream_t)stream);
 }
 
-void prof_end(int cls, double bytes, void *stream) {
+void prof_end(int cls, double bytes, void *stream, double impl, double terms) {
     if (!g_prof_on || !g_pending) return;
     std::lock_guard<std::mutex> lk(g_prof_mu);
     cudaEvent_t b = ev_get();
     cudaEventRecord(b, (cudaStream_t)stream);
-    g_prof.push_back({cls, g_pending, b, bytes});
+    g_prof.push_back({cls, g_pending, b, bytes, impl < 0 ? bytes : impl, terms});
     g_pending = nullptr;
 }
 
@@ -982,6 +982,29 @@ sg2v_status sg2v_profile_enable(int32_t on) {
     for (auto &r : g_prof) { g_ev_pool.push_back(r.a); g_ev_pool.push_back(r.b); }
     g_prof.clear();
     g_prof_on = on != 0;
+    return SG2V_OK;
+}
+
+sg2v_status sg2v_profile_read_launches(int64_t cap, int32_t *cls, double *ms, double *alg_bytes,
+                                       double *impl_bytes, double *ema_terms, int64_t *n_out) {
+    if (!n_out || (cap > 0 && (!cls || !ms || !alg_bytes || !impl_bytes || !ema_terms))) {
+        set_error("NULL argument");
+        return SG2V_EINVAL;
+    }
+    std::lock_guard<std::mutex> lk(g_prof_mu);
+    *n_out = (int64_t)g_prof.size();
+    for (int64_t q = 0; q < cap && q < (int64_t)g_prof.size(); ++q) {
+        const ProfRec &r = g_prof[(size_t)q];
+        cudaError_t e = cudaEventSynchronize(r.b);
+        if (e != cudaSuccess) return cuda_fail("profile event", e);
+        float t = 0.f;
+        cudaEventElapsedTime(&t, r.a, r.b);
+        cls[q] = r.cls;
+        ms[q] = t;
+        alg_bytes[q] = r.bytes;
+        impl_bytes[q] = r.impl;
+        ema_terms[q] = r.terms;
+    }
     return SG2V_OK;
 }
 

@@ -101,7 +101,9 @@ __device__ __forceinline__ void group_sync(int g) {
     } else if constexpr (GT == 32) {
         __syncwarp();
     } else if constexpr (GT == 256) {
-        __syncthreads();
+        // named barrier 1 of 256 threads (not bar 0): the bulk-staged kernel runs a
+        // producer warp beside the 256 consumer threads, which must not join
+        asm volatile("bar.sync 1, 256;" ::: "memory");
     } else {
         asm volatile("bar.sync %0, %1;" ::"r"(g + 1), "r"(GT) : "memory");
     }
@@ -138,6 +140,42 @@ __device__ __forceinline__ T vget(const uint4 &v, int e) {
 template <typename T>
 __device__ __forceinline__ void vset(uint4 &v, int e, T x) {
     reinterpret_cast<T *>(&v)[e] = x;
+}
+
+// ---- mbarrier + bulk-copy (TMA engine, non-tensor) helpers ----
+__device__ __forceinline__ uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void fence_mbar_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t *bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+// global -> shared bulk copy of `bytes` (multiple of 16, both ends 16-B aligned), completion
+// counted on `bar` (complete_tx), L2 eviction policy `pol` (createpolicy)
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar, uint64_t pol) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
+        : "memory");
+}
+__device__ __forceinline__ uint4 lds16(const void *p) {
+    uint4 r;
+    asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "r"(smem_u32(p)));
+    return r;
 }
 
 int num_sms();

@@ -399,7 +399,7 @@ int launch_step(const Graph &g, const Plan &pl, const Step &st, const uint8_t *c
         else
             top_leaf_kernel<u64, u64><<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(
                 g.n, g.d_rowptr, g.d_col, colors, (const u64 *)src, st.ldp, srch, idx, (u64 *)rowval);
-        prof_end(3, st.alg_bytes, stream);
+        prof_end(3, st.alg_bytes, stream, st.impl_bytes, 0.0);
         return (int)cudaGetLastError();
     }
     StepArgs A;
@@ -430,7 +430,7 @@ int launch_step(const Graph &g, const Plan &pl, const Step &st, const uint8_t *c
     if (pl.prec == SG2V_F32) rc = launch_step_gt<float, double>(A, st.gt, stream);
     else if (pl.prec == SG2V_F64) rc = launch_step_gt<double, double>(A, st.gt, stream);
     else rc = launch_step_gt<u64, u64>(A, st.gt, stream);
-    prof_end(cls, st.alg_bytes, stream);
+    prof_end(cls, st.alg_bytes, stream, st.impl_bytes, st.ema_terms);
     return rc;
 }
 

@@ -214,6 +214,64 @@ static int64_t table_width(Layout L, int k, int size) {
     return L == LAYOUT_DENSE ? binom(k, size) : binom(k - 1, size - 1);
 }
 
+// Arena placement of buffers with the given alloc/free sequence (buffer id, alloc?).
+// Returns the arena size and writes each buffer's offset (256-B aligned).
+template <typename EvT>
+static std::vector<std::pair<int, bool>> events_to_pairs(const std::vector<EvT> &e) {
+    std::vector<std::pair<int, bool>> out;
+    for (const auto &x : e) out.push_back({x.buf, x.alloc});
+    return out;
+}
+
+static int64_t place_one(std::vector<Buffer> &bufs, const std::vector<std::pair<int, bool>> &ev,
+                         const std::vector<int> &side_hint, bool two_sided) {
+    std::vector<int> side(bufs.size(), 0);
+    std::vector<int64_t> soff(bufs.size(), 0);                // offset from the side's origin
+    std::vector<std::pair<int64_t, int64_t>> live[2];          // (offset, bytes) per side
+    int64_t ext[2] = {0, 0}, H = 0;
+    for (const auto &e : ev) {
+        const int b = e.first;
+        const int64_t bytes = round_up(std::max<int64_t>(bufs[b].bytes, 1), 256);
+        if (e.second) {
+            int sd = 0;
+            if (two_sided && side_hint[b] >= 0) sd = 1 - side[side_hint[b]];
+            side[b] = sd;
+            auto &L = live[sd];
+            std::sort(L.begin(), L.end());
+            int64_t pos = 0;
+            for (auto &iv : L) {
+                if (iv.first - pos >= bytes) break;
+                pos = std::max(pos, iv.first + iv.second);
+            }
+            L.push_back({pos, bytes});
+            soff[b] = pos;
+            ext[sd] = 0;
+            for (auto &iv : L) ext[sd] = std::max(ext[sd], iv.first + iv.second);
+            H = std::max(H, ext[0] + ext[1]);
+        } else {
+            auto &L = live[side[b]];
+            for (size_t q = 0; q < L.size(); ++q)
+                if (L[q].first == soff[b]) { L.erase(L.begin() + q); break; }
+            int64_t x = 0;
+            for (auto &iv : L) x = std::max(x, iv.first + iv.second);
+            ext[side[b]] = x;
+        }
+    }
+    H = round_up(H, 256);
+    for (size_t b = 0; b < bufs.size(); ++b)
+        bufs[b].offset = side[b] == 0 ? soff[b] : H - soff[b] - round_up(std::max<int64_t>(bufs[b].bytes, 1), 256);
+    return H;
+}
+
+static int64_t place_arena(std::vector<Buffer> &bufs, const std::vector<std::pair<int, bool>> &ev,
+                           const std::vector<int> &side_hint) {
+    std::vector<Buffer> one = bufs, two = bufs;
+    const int64_t h1 = place_one(one, ev, side_hint, false);
+    const int64_t h2 = place_one(two, ev, side_hint, true);
+    bufs = h2 < h1 ? two : one;
+    return std::min(h1, h2);
+}
+
 // Build steps, schedule, buffers and the model for one chain.
 static bool plan_chain(const Template &t, const Chain &c, int root, int64_t n, int64_t nnz,
                        sg2v_precision prec, Layout L, Plan &pl, const std::set<std::string> &proj = {}) {
@@ -358,26 +416,28 @@ static bool plan_chain(const Template &t, const Chain &c, int root, int64_t n, i
         uses[pkey(v)]++;
     }
 
-    // --- first-fit arena over the schedule ---
+    // --- table arena over the schedule ---
+    // Buffers are recorded as alloc / free events in schedule order and placed after
+    // the loop (place_arena): one-sided first fit, or two-sided (a step's output goes
+    // to the side opposite its passive input, so a chain of steps ping-pongs between
+    // the two ends instead of leaving holes too small for the next, wider table);
+    // the smaller arena wins.
     std::map<std::string, int> class_buf;   // canon -> buffer
     std::vector<int> node_buf(pl.nodes.size(), -1);
-    std::vector<std::pair<int64_t, int64_t>> live;  // (offset, bytes)
-    int64_t arena = 0;
-    auto alloc = [&](int64_t bytes) -> int64_t {
-        int64_t pos = 0;
-        std::sort(live.begin(), live.end());
-        for (auto &iv : live) {
-            if (iv.first - pos >= bytes) break;
-            pos = std::max(pos, round_up(iv.first + iv.second, 256));
-        }
-        live.push_back({pos, bytes});
-        arena = std::max(arena, pos + bytes);
-        return pos;
+    struct Ev { int buf; bool alloc; };
+    std::vector<Ev> events;
+    std::vector<int> side_hint;             // per buffer: the buffer whose side it should avoid (-1: none)
+    auto alloc = [&](int64_t bytes, int avoid) -> int64_t {
+        Buffer b;
+        b.bytes = bytes;
+        b.offset = 0;
+        pl.bufs.push_back(b);
+        side_hint.push_back(avoid);
+        events.push_back({(int)pl.bufs.size() - 1, true});
+        return 0;
     };
     auto release = [&](int b) {
-        if (b < 0) return;
-        for (size_t q = 0; q < live.size(); ++q)
-            if (live[q].first == pl.bufs[b].offset) { live.erase(live.begin() + q); break; }
+        if (b >= 0) events.push_back({b, false});
     };
 
     double model = 0.0, alg_total = 0.0;
@@ -419,26 +479,21 @@ static bool plan_chain(const Template &t, const Chain &c, int root, int64_t n, i
         st.buf_p = class_buf.count(st.canon_p) ? class_buf[st.canon_p] : -1;
         if (st.src == SRC_HIST && !anch) pl.need_hist = true;
         if (st.plain_out) {
-            Buffer b;
-            b.bytes = n * st.lds * pl.elem;
-            b.offset = alloc(b.bytes);
-            pl.bufs.push_back(b);
+            alloc(n * st.lds * pl.elem, st.buf_p);
             st.buf_out = (int)pl.bufs.size() - 1;
             node_buf[v] = st.buf_out;
             class_buf[st.canon_out] = st.buf_out;
         }
         if (st.proj_out) {
-            Buffer b;
-            b.bytes = n * st.ldsx * pl.elem;
-            b.offset = alloc(b.bytes);
-            pl.bufs.push_back(b);
+            alloc(n * st.ldsx * pl.elem, st.buf_p);
             st.buf_outx = (int)pl.bufs.size() - 1;
             class_buf[st.canon_out + "|x"] = st.buf_outx;
         }
         if (!st.self_a && --uses[st.canon_a] == 0) release(st.buf_a);
         if (--uses[st.canon_p] == 0) release(st.buf_p);
 
-        // algorithmic bytes (useful columns only) and the model (sector-rounded)
+        // impl bytes (the implemented layout's compulsory traffic), the model
+        // (sector-rounded) and below the method's algorithmic bytes
         double bytes = 0.0, mbytes = 0.0;
         const bool top_leaf = st.top && st.comb == COMB_ACTIVE_LEAF;
         const double hsrc = anch ? n * (double)round_up(k, 4) * 4.0 : n * (double)k * E;
@@ -475,13 +530,31 @@ static bool plan_chain(const Template &t, const Chain &c, int root, int64_t n, i
         else
             st.nterms = 1;
         st.ema_terms = (st.comb == COMB_GENERAL) ? (double)n * (double)st.cs * (double)st.nterms : 0.0;
-        st.alg_bytes = bytes;
+        st.impl_bytes = bytes;
+        {
+            // SURVEY §8(d) per-step bytes of the method, independent of plain vs projected
+            // tables: useful gather (anchored: each live edge carries the C(k-2,p-1) sets
+            // avoiding c(i); dense: C(k,p)), CSR + per-row metadata, M_a, and the output
+            // written once at plain width (top: one 8-B value per vertex)
+            double u = 0.0;
+            if (top_leaf) {
+                u = st.src == SRC_GATHER ? nnz * 4.0 + nnz * live_frac * E + n * 9.0 : hsrc + n * 9.0;
+            } else {
+                const double useful_cols = anch ? (double)binom(k - 2, st.p - 1) : (double)binom(k, st.p);
+                u = st.src == SRC_GATHER ? nnz * 4.0 + nnz * live_frac * useful_cols * E + n * (12.0 + (anch ? 4.0 * k : 0.0))
+                                         : hsrc;
+                u += (st.comb == COMB_GENERAL && !st.self_a) ? n * (double)table_width(L, k, st.a) * E : n * 1.0;
+                u += st.top ? n * 8.0 : n * (double)table_width(L, k, st.s) * E;
+            }
+            st.alg_bytes = u;
+        }
         st.gt = pick_gt(std::max({st.ldp, st.ldb, st.lds, st.comb == COMB_GENERAL ? st.lda : 0}), vn);
         model += mbytes / kHbm + st.ema_terms / kTermRate;
-        alg_total += bytes;
+        alg_total += st.alg_bytes;
+        pl.impl_bytes_total += bytes;
         pl.steps.push_back(st);
     }
-    pl.tables_bytes = round_up(arena, 256);
+    pl.tables_bytes = place_arena(pl.bufs, events_to_pairs(events), side_hint);
     pl.ldh = round_up(k, vn);
     pl.kp = round_up(k, 4);
     pl.hist_bytes = pl.need_hist ? n * pl.ldh * pl.elem : 0;
@@ -489,11 +562,13 @@ static bool plan_chain(const Template &t, const Chain &c, int root, int64_t n, i
         double hb = nnz * 4.0 + nnz * 1.0 + n * 12.0 + n * (double)k * E;
         model += (nnz * 4.0 + nnz * 32.0 + pl.hist_bytes) / kHbm;
         alg_total += hb;
+        pl.impl_bytes_total += hb;
     }
     if (anch) {  // colour counts + colour-bucketed CSR, once per colouring
         double bb = 2.0 * nnz * 4.0 + nnz * 4.0 + n * 16.0 + n * (double)pl.kp * 4.0;
         model += (bb + nnz * 32.0) / kHbm;
         alg_total += bb;
+        pl.impl_bytes_total += bb;
     }
     pl.model_time = model;
     pl.alg_bytes_total = alg_total;
@@ -757,7 +832,8 @@ std::string Plan::describe() const {
       << ",\"precision\":\"" << (prec == SG2V_F32 ? "f32" : prec == SG2V_F64 ? "f64" : "u64") << "\""
       << ",\"need_hist\":" << (need_hist ? "true" : "false") << ",\"hist_bytes\":" << hist_bytes
       << ",\"tables_bytes\":" << tables_bytes << ",\"workspace_bytes\":" << ws_bytes
-      << ",\"model_seconds\":" << model_time << ",\"alg_bytes\":" << alg_bytes_total << ",\"steps\":[";
+      << ",\"model_seconds\":" << model_time << ",\"alg_bytes\":" << alg_bytes_total
+      << ",\"impl_bytes\":" << impl_bytes_total << ",\"steps\":[";
     for (size_t i = 0; i < steps.size(); ++i) {
         const Step &s = steps[i];
         o << (i ? "," : "") << "{\"s\":" << s.s << ",\"a\":" << s.a << ",\"p\":" << s.p
@@ -769,7 +845,8 @@ std::string Plan::describe() const {
           << ",\"self\":" << (s.self_a ? "true" : "false")
           << ",\"proj_out\":" << (s.proj_out ? "true" : "false") << ",\"proj_p\":" << (s.proj_p ? "true" : "false")
           << ",\"plain_out\":" << (s.plain_out ? "true" : "false") << ",\"ldsx\":" << s.ldsx
- << ",\"gt\":" << s.gt << ",\"alg_bytes\":" << s.alg_bytes << ",\"ema_terms\":" << s.ema_terms << "}";
+ << ",\"gt\":" << s.gt << ",\"alg_bytes\":" << s.alg_bytes << ",\"impl_bytes\":" << s.impl_bytes
+      << ",\"ema_terms\":" << s.ema_terms << "}";
     }
     o << "]}";
     return o.str();

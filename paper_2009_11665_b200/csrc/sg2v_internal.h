@@ -80,7 +80,10 @@ struct Step {
     int64_t omap_off = -1;                 // projected output: write map (int32 offset)
     std::string canon_out, canon_a, canon_p;  // rooted classes of T_s, T_a, T_p (table sharing)
     int gt = 32;                           // threads per row group (step kernel)
-    double alg_bytes = 0.0;                // algorithmic HBM bytes
+    double alg_bytes = 0.0;                // algorithmic HBM bytes of the METHOD:
+                                           //   useful gather + CSR + M_a + plain-width output (layout-independent)
+    double impl_bytes = 0.0;               // compulsory bytes of the implemented layout (plain-width gathers
+                                           //   from plain sources, projected-copy writes)
     double ema_terms = 0.0;
 };
 
@@ -113,7 +116,7 @@ struct Plan {
     int32_t *d_index = nullptr;   // device copy (owned by the template's cache)
     int top_leaf_col_off = -1;    // idx offset of topcol[k] when the top step is leaf-active
     double model_time = 0.0;
-    double alg_bytes_total = 0.0;
+    double alg_bytes_total = 0.0, impl_bytes_total = 0.0;
     int64_t hist_bytes = 0;
     bool allow_proj = true;       // planner may choose exclusion-projected tables
     std::vector<std::string> proj_cands;  // classes that could be projected (planning)
@@ -173,6 +176,7 @@ int graph_validate(const Graph &g, int *bad, void *stream);
 
 // profiling (api.cpp)
 void prof_begin(int cls, void *stream);
-void prof_end(int cls, double bytes, void *stream);
+// alg: SURVEY §8(d) bytes of the launch; impl: the implemented layout's bytes; terms: eMA terms
+void prof_end(int cls, double alg, void *stream, double impl = -1.0, double terms = 0.0);
 
 }  // namespace sg2v

@@ -55,7 +55,8 @@ SYMBOLS = ["sg2v_graph_load_csr", "sg2v_graph_free", "sg2v_template_build", "sg2
            "sg2v_count", "sg2v_count_ex", "sg2v_colorize", "sg2v_plan_describe", "sg2v_plan_describe_n", "sg2v_profile_enable",
            "sg2v_profile_read", "sg2v_last_error", "sg2v_version", "sg2v_count_batch",
            "sg2v_workspace_bytes_batch", "sg2v_comm_unique_id", "sg2v_comm_init_nccl", "sg2v_comm_init_callback",
-           "sg2v_comm_free", "sg2v_graph_load_partition", "sg2v_estimate"]
+           "sg2v_comm_free", "sg2v_graph_load_partition", "sg2v_estimate",
+           "sg2v_profile_read_launches"]
 
 ALLGATHER_FN = ctypes.CFUNCTYPE(ctypes.c_int32, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_uint64, ctypes.c_void_p)
 
@@ -95,6 +96,7 @@ def lib():
         L.sg2v_plan_describe.argtypes = [vp, vp, ctypes.c_int, vp, u64, P(u64)]
         L.sg2v_plan_describe_n.argtypes = [i64, i64, vp, ctypes.c_int, vp, u64, P(u64)]
         L.sg2v_estimate.argtypes = [vp, i64, vp, P(ctypes.c_double)]
+        L.sg2v_profile_read_launches.argtypes = [i64, vp, vp, vp, vp, vp, P(i64)]
         L.sg2v_profile_enable.argtypes = [i32]
         L.sg2v_profile_read.argtypes = [vp, vp, vp]
         L.sg2v_last_error.restype = ctypes.c_char_p
@@ -104,7 +106,7 @@ def lib():
                      "sg2v_plan_describe", "sg2v_plan_describe_n", "sg2v_profile_enable", "sg2v_profile_read",
                      "sg2v_count_batch", "sg2v_workspace_bytes_batch", "sg2v_comm_unique_id",
                      "sg2v_comm_init_nccl", "sg2v_comm_init_callback", "sg2v_graph_load_partition",
-                     "sg2v_estimate"):
+                     "sg2v_estimate", "sg2v_profile_read_launches"):
             getattr(L, name).restype = ctypes.c_int
         _lib = L
     return _lib
@@ -472,6 +474,19 @@ def profile_read():
     _check(lib().sg2v_profile_read(launches.ctypes.data, ms.ctypes.data, by.ctypes.data))
     return {c: {"launches": int(launches[i]), "ms": float(ms[i]), "bytes": float(by[i])}
             for i, c in enumerate(KERNEL_CLASSES)}
+
+
+def profile_read_launches():
+    """Per-launch records: list of dicts {cls, ms, alg_bytes, impl_bytes, ema_terms}."""
+    n = ctypes.c_int64()
+    _check(lib().sg2v_profile_read_launches(0, None, None, None, None, None, ctypes.byref(n)))
+    m = int(n.value)
+    cls = np.zeros(max(m, 1), np.int32)
+    ms, ab, ib, te = (np.zeros(max(m, 1), np.float64) for _ in range(4))
+    _check(lib().sg2v_profile_read_launches(m, cls.ctypes.data, ms.ctypes.data, ab.ctypes.data, ib.ctypes.data,
+                                            te.ctypes.data, ctypes.byref(n)))
+    return [{"cls": KERNEL_CLASSES[int(cls[q])], "ms": float(ms[q]), "alg_bytes": float(ab[q]),
+             "impl_bytes": float(ib[q]), "ema_terms": float(te[q])} for q in range(m)]
 
 
 def version() -> str:

@@ -1,14 +1,14 @@
 """GPU parity at BASELINE.json's full sizes, in the launch configuration bench.py times.
 
-* Configs the CPU oracle can finish (u5-2, u7-2, u12-1 on RMAT-1M-like; u5-2, u7-2 on
-  Miami-like; u10-2 on Orkut-like): compared with oracle values written by
-  tools/make_golden_big.py (tests/golden/big_configs.json; calls only oracle/).
-  U64 bit-exact; F64 bit-exact below 2^53 else rel 1e-12; F32 rel 1e-4.
-* u15-1 (the bench workload) and u17 on RMAT-1M-like, where the oracle's dense
-  fp64 tables do not fit host RAM: properties that hold at any size (SURVEY §8(c)
-  pin 5): the exact U64 residue is the same for different roots / cut orders
-  (different kernels, index tables and schedules) and for the dense vs the
-  root-colour-anchored layout; F32 agrees with F64 to 1e-4.
+* Configs the CPU oracle finishes (u5-2, u7-2, u12-1 and u15-1 — the bench workload,
+  colourings j = 0 and j = 5, a colouring the bench times — on RMAT-1M-like; u5-2,
+  u7-2 on Miami-like; u10-2 on Orkut-like): compared with oracle values written by
+  tools/make_golden_big.py (tests/golden/big_configs.json; calls only oracle/; u15-1
+  ran on the GPU box's host, 16 threads, ~109 GB peak).  U64 bit-exact; F64 bit-exact
+  below 2^53 else rel 1e-12; F32 rel 1e-4; per-vertex values on sampled rows too.
+* u17 on RMAT-1M-like, where the oracle's dense tables (~290 GB) exceed the host:
+  properties that hold at any size (SURVEY §8(c) pin 5): the exact U64 residue is the
+  same for different roots / cut orders.
 """
 import json
 import math
@@ -61,8 +61,14 @@ def _count(G, T, prec, layout="anchored", j=0):
 CASES = json.load(open(GOLD))["cases"]
 
 
-@pytest.mark.parametrize("case", CASES, ids=[f"{c['graph']}-{c['template']}" for c in CASES])
+def _case_id(c):
+    return f"{c['graph']}-{c['template']}" + (f"-j{c['j']}" if c["j"] else "")
+
+
+@pytest.mark.parametrize("case", CASES, ids=[_case_id(c) for c in CASES])
 def test_big_config_vs_oracle(case):
+    """Totals in the launch configuration bench.py times (the planner's default plan,
+    workspace_bytes-sized workspace), against the oracle run on the full graph."""
     g, G = _graph(case["graph"])
     assert g.nnz == case["graph_stats"]["nnz"] and g.n == case["graph_stats"]["n"]
     e = TEMPLATES[case["template"]]
@@ -70,6 +76,8 @@ def test_big_config_vs_oracle(case):
     layouts = ("anchored", "dense") if case["k"] <= 7 else ("anchored",)
     for layout in layouts:
         assert int(_count(G, T, "u64", layout, case["j"])) == int(case["colorful_u64"]), layout
+        if "colorful_f64" not in case:
+            continue
         f64 = _count(G, T, "f64", layout, case["j"])
         if case["max_intermediate"] < 2 ** 53:
             assert f64 == case["colorful_f64"]
@@ -77,6 +85,41 @@ def test_big_config_vs_oracle(case):
             assert math.isclose(f64, case["colorful_f64"], rel_tol=1e-12)
         f32 = _count(G, T, "f32", layout, case["j"])
         assert math.isfinite(f32) and math.isclose(f32, case["colorful_f64"], rel_tol=1e-4)
+
+
+ROW_CASES = [c for c in CASES if "rows" in c]
+
+
+@pytest.mark.parametrize("case", ROW_CASES, ids=[_case_id(c) for c in ROW_CASES])
+def test_big_config_rows_vs_oracle(case):
+    """Per-vertex values (embeddings with the template root at vertex i) on the oracle's
+    sampled rows (the 64 highest-degree vertices + uniform picks), GPU rooted where the
+    oracle was rooted: U64 bit-exact, F64 rel 1e-12, F32 rel 1e-4 per element."""
+    g, G = _graph(case["graph"])
+    e = TEMPLATES[case["template"]]
+    T = sg.template_build(_k(e), e, root_hint=case["root"])
+    rows = np.array(case["rows"], dtype=np.int64)
+    for prec in ("u64", "f64", "f32"):
+        key = "rows_u64" if prec == "u64" else "rows_f64"
+        if key not in case:
+            continue
+        dt = torch.int64 if prec == "u64" else torch.float64
+        rv = torch.zeros(g.n, dtype=dt, device="cuda")
+        ws = sg.Workspace(sg.workspace_bytes(G, T, prec))
+        _, c = sg.count(G, T, n_iter=1, seed=1, iter_offset=case["j"], precision=prec, workspace=ws, row_values=rv,
+                        allow_overflow=prec == "f32")
+        del ws
+        r = rv.cpu().numpy()[rows]
+        torch.cuda.empty_cache()
+        if prec == "u64":
+            assert int(c[0]) == int(case["colorful_u64"])
+            assert [int(x) for x in r.view(np.uint64)] == [int(x) for x in case[key]]
+        else:
+            want = np.array(case[key], dtype=np.float64)
+            zero = want == 0
+            assert np.all(r[zero] == 0)
+            rel = np.abs(r[~zero] - want[~zero]) / want[~zero]
+            assert float(rel.max(initial=0.0)) <= (1e-12 if prec == "f64" else 1e-4), (prec, float(rel.max()))
 
 
 def test_u15_bench_workload_invariants():

@@ -7,7 +7,8 @@ from sg2v_inputs import rmat_1m_like, TEMPLATES
 name, prec = sys.argv[1], sys.argv[2]
 layout = sys.argv[3] if len(sys.argv) > 3 else "anchored"
 n_iter = int(sys.argv[4]) if len(sys.argv) > 4 else 1
-g = rmat_1m_like()
+scale = int(sys.argv[5]) if len(sys.argv) > 5 else 20
+g = rmat_1m_like(scale=scale)
 torch.cuda.set_device(0)
 G = sg.graph_load_csr(g.n, g.row_offsets, g.col_indices)
 e = TEMPLATES[name]; k = 1 + max(max(x) for x in e)
