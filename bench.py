@@ -52,6 +52,10 @@ def _args():
                    help="replicas: colourings sharded over ranks (weak); vertex: every colouring's tables "
                         "row-partitioned over ranks with NCCL column-tile all-gathers (strong, SURVEY 8(e) V)")
     p.add_argument("--col-tile", type=int, default=0)
+    p.add_argument("--graph", default="rmat1m", choices=["rmat1m", "gs22", "miami", "orkut"],
+                   help="rmat1m: RMAT-1M-like at --scale (D4); gs22: Graph500-like scale 22 (D5a); miami (D2); orkut (D3)")
+    p.add_argument("--no-balance", action="store_true",
+                   help="vertex mode: uniform row blocks of the input ids instead of the degree-dealt relabelling")
     return p.parse_args()
 
 
@@ -62,8 +66,17 @@ def _template(name):
 
 
 def _workload_name(args, g):
+    if args.graph != "rmat1m":
+        return f"{args.template} on {g.name} (n={g.n}, nnz={g.nnz})"
     return (f"{args.template} on RMAT-1M-like (scale {args.scale}, RMAT(0.45,0.22,0.22,0.11), "
             f"n={g.n}, nnz={g.nnz})")
+
+
+def _load_graph(args):
+    from sg2v_inputs import BIG_GRAPHS, rmat_1m_like
+    if args.graph == "rmat1m":
+        return rmat_1m_like(scale=args.scale, seed=args.seed)
+    return BIG_GRAPHS[args.graph]()
 
 
 # --------------------------------------------------------------------------- clocks
@@ -368,7 +381,7 @@ def run_sg2v(args):
 
     build()
     k, edges = _template(args.template)
-    g = rmat_1m_like(scale=args.scale, seed=args.seed)
+    g = _load_graph(args)
     stats = degree_stats(g)
     # pinned host copies for the e2e leg
     ro_h = torch.from_numpy(g.row_offsets).pin_memory()
@@ -385,7 +398,8 @@ def run_sg2v(args):
 
     overflow = []  # colourings whose F32 count overflowed (EOVERFLOW), reported in the line
 
-    def count(GG, n_iter, off, stride=1, wsp=ws):
+    def count(GG, n_iter, off, stride=1, wsp=None):
+        wsp = ws if wsp is None else wsp
         try:
             return sg.count(GG, T, n_iter=n_iter, seed=args.seed, iter_offset=off, iter_stride=stride,
                             precision=args.precision, workspace=wsp, layout=args.layout)
@@ -433,7 +447,7 @@ def run_sg2v(args):
     e2e_steps = args.e2e_steps if args.e2e_steps is not None else args.steps
     del G
     ws_bytes = ws.nbytes
-    del ws
+    ws = None  # (count() looks `ws` up at call time: the timed e2e steps allocate their own)
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
@@ -500,7 +514,9 @@ def run_sg2v(args):
 
 
 def run_vertex(args):
-    """--mode vertex: 1D vertex partition of every table across the ranks (capacity mode)."""
+    """--mode vertex: 1D vertex partition of every table across the ranks (capacity mode,
+    SURVEY §8(e) V).  Rows are dealt to the rank blocks by degree (sg2v_partition_relabel,
+    colours keyed by the input ids) unless --no-balance."""
     import numpy as np
     import torch
     import torch.distributed as dist
@@ -511,20 +527,31 @@ def run_vertex(args):
     dev = _setup_dist(world, local)
     import paper_2009_11665_b200 as sg
     from paper_2009_11665_b200.build import build
-    from sg2v_inputs import degree_stats, rmat_1m_like
+    from sg2v_inputs import degree_stats
 
     build()
     k, edges = _template(args.template)
-    g = rmat_1m_like(scale=args.scale, seed=args.seed)
+    g = _load_graph(args)
     stats = degree_stats(g)
     b, nl = sg.partition_rows(g.n, rank, world)
-    ro = np.ascontiguousarray(g.row_offsets[b:b + nl + 1] - g.row_offsets[b])
-    ci = np.ascontiguousarray(g.col_indices[g.row_offsets[b]:g.row_offsets[b + nl]])
+    if args.no_balance:
+        ro_all, ci_all, oon = g.row_offsets, g.col_indices, None
+    else:
+        oon, ro_all, ci_all = sg.partition_relabel(g.row_offsets, g.col_indices, world)
+    ro = np.ascontiguousarray(ro_all[b:b + nl + 1] - ro_all[b])
+    ci = np.ascontiguousarray(ci_all[ro_all[b]:ro_all[b + nl]])
     uid = [sg.Comm.unique_id() if rank == 0 else None]
     if world > 1:
         dist.broadcast_object_list(uid, src=0)
     comm = sg.Comm.nccl(uid[0], rank, world)
-    Gp = sg.graph_load_partition(g.n, b, nl, ro, ci)
+
+    def load():
+        G = sg.graph_load_partition(g.n, b, nl, ro, ci)
+        if oon is not None:
+            sg.graph_set_vertex_ids(G, oon)
+        return G
+
+    Gp = load()
     T = sg.template_build(k, edges)
     kw = dict(seed=args.seed, precision=args.precision, comm=comm, col_tile=args.col_tile, allow_overflow=True)
     for t in range(args.warmup):
@@ -554,7 +581,7 @@ def run_vertex(args):
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
     for t in range(e2e_steps):
-        Ge = sg.graph_load_partition(g.n, b, nl, ro, ci)
+        Ge = load()
         sg.count(Ge, T, n_iter=1, iter_offset=args.warmup + args.steps + t, **kw)
         Ge.free()
     e1.record(stream)
@@ -565,29 +592,37 @@ def run_vertex(args):
     e2e_value = float(e_max.item()) / max(e2e_steps, 1)
     comm.free()
     if rank == 0:
-        peaks = {}
-        try:
-            peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
-        except Exception:
-            pass
+        peaks, psrc = _peaks()
         peak = float(peaks.get("hbm_gbs", 6650.0))
         dom = "step"
         achieved = prof[dom]["bytes"] / (prof[dom]["ms"] / 1e3) / 1e9 if prof[dom]["ms"] > 0 else 0.0
         launches = sum(v["launches"] for v in prof.values()) + prof["reduce"]["launches"]
+        # NVLink: bytes each rank receives per colouring in the whole-row exchange (the
+        # plain anchored plan on nl rows: (W-1)·nl·ldp·E per gather step), over the
+        # colouring's time — a lower bound on the link rate while exchanging
+        plain = sg.plan_describe_n(-(-g.n // world), max(g.nnz // world, 1), T, args.precision, "anchored_plain")
+        E = plain["elem"]
+        nlr = -(-g.n // world)
+        recv = sum((world - 1) * nlr * st["ldp"] * E for st in plain["steps"] if st["src"] == "gather")
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": value * 1e3, "higher_is_better": False, "scaling": "strong",
                 "vs_baseline": None, "dtype": args.precision, "data": "synthetic",
                 "config": {"workload": _workload_name(args, g), "template": args.template, "k": k,
-                           "precision": args.precision, "layout": "anchored", "graph": stats,
+                           "precision": args.precision, "layout": "anchored (plain tables)", "graph": stats,
                            "parallelism": f"vertex{world}", "rows_per_rank": nl, "col_tile": args.col_tile,
+                           "balanced_relabel": oon is not None,
                            "l2": "inputs larger than L2; no flush"},
                 "estimate": est, "colorful_first": float(c[0]),
                 "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(ro.nbytes + ci.nbytes),
                         "d2h_bytes_per_step": 8},
                 "gpu_launches": int(launches),
                 "kernel_ms_per_step": {kk: v["ms"] / args.steps for kk, v in prof.items()},
-                "roofline": {"bound": "hbm", "kernel": "step (tile gathers of rank 0)", "achieved": achieved,
-                             "peak": peak, "unit": "GB/s", "frac": achieved / peak, "traffic": None},
+                "roofline": {"bound": "hbm", "kernel": "step (rank 0)", "achieved": achieved,
+                             "peak": peak, "unit": "GB/s", "frac": achieved / peak, "traffic": None,
+                             "peak_source": psrc},
+                "nvlink": {"recv_bytes_per_colouring_per_rank": recv,
+                           "achieved_GBps_lower_bound": recv / value / 1e9 if value > 0 else 0.0,
+                           "peak_GBps": 900.0, "frac_lower_bound": recv / value / 1e9 / 900.0 if value > 0 else 0.0},
                 "clocks": clk.summary()}
         print(json.dumps(line), flush=True)
     if world > 1:

@@ -225,6 +225,29 @@ sg2v_status sg2v_graph_load_partition(int64_t n_global, int64_t row_begin, int64
                                       int64_t nnz, uint32_t flags, sg2v_graph **out);
 
 /*
+ * Balanced relabelling for the vertex-partitioned mode ("blocks balanced
+ * by nnz + n·c_max weight, after a random relabel; colours stay keyed by the input id").
+ * Blocks keep the contract above (rank r owns new ids [r·nl, r·nl + n_local)); the
+ * vertices are dealt to the blocks by degree, heaviest first, in snake order, so every
+ * block holds ~nnz/world edges (the n·c_max table term is equal by construction).
+ *   n, row_offsets[n+1], col_indices[nnz]  the input CSR (host)
+ *   old_of_new[n]   out: input id of new vertex u
+ *   ro_out[n+1], ci_out[nnz]  out: the relabelled CSR (rows sorted)
+ * Pass old_of_new (the slice-independent map) to sg2v_graph_set_vertex_ids of every
+ * rank's partition so colours, hence every count, equal the input graph's.
+ */
+sg2v_status sg2v_partition_relabel(int64_t n, const int64_t *row_offsets, const int32_t *col_indices, int32_t world,
+                                   int32_t *old_of_new, int64_t *ro_out, int32_t *ci_out);
+
+/*
+ * Vertex ids for colouring (P:150 leaves the RNG open; SURVEY §8(c) "RNG": colours are
+ * keyed by the INPUT vertex id, so a relabelled graph must carry the original ids):
+ * vertex v of g is coloured COLOR(seed, j, orig_ids[v], k).  count = n, or n_global
+ * for a partition (host array, copied).  count = 0 clears the map.
+ */
+sg2v_status sg2v_graph_set_vertex_ids(sg2v_graph *g, const int32_t *orig_ids, int64_t count);
+
+/*
  * sg2v_colorize — kernel a1 alone: writes
  * COLOR(seed, j, v, k) for v in [0,n) to the DEVICE array colors_out (uint8[n])
  * on `stream` (cudaStream_t or NULL).  For parity tests of the colouring.

@@ -133,6 +133,7 @@ struct AStepArgs {
     int bsrc_global;    // stage 1 = copy the completed B row from bg
     char *bg;           // [n_local][ldb] B rows (tile_mode / bsrc_global)
     int *ovf;           // F32 overflow flag of this sg2v_count call (in its workspace)
+    int64_t n_heavy;    // rows [0, n_heavy) of `order` have >= 2^kHeavyLog2 neighbours
 };
 
 // F32 overflow flag (AStepArgs::ovf, one int in the calling sg2v_count's workspace, so
@@ -518,6 +519,133 @@ __global__ void __launch_bounds__(256, AStepMinBlocks<U, V, MODE>::value) astep_
 }
 
 // ---------------------------------------------------------------------------
+// heavy rows of narrow steps (north_star "CTA-per-heavy-row"): a row
+// with thousands of neighbours walked by the small row group of a narrow step (4-32
+// lanes) would run for milliseconds after every other row is done.  The rows with
+// degree >= 2^kHeavyLog2 — a prefix of the degree-descending order — are taken first
+// by this kernel, one CTA per row: the 256 threads form NG = 256/SG sub-groups of SG
+// lanes (lane l owns 16-B vectors l, l+SG, ...), sub-group g takes the neighbours
+// c ≡ g (mod NG) of each colour bucket, and the NG partial sums are added in a fixed
+// order (g = 0..NG-1) before the push — deterministic, no atomics.  Same stage 2.
+// ---------------------------------------------------------------------------
+static constexpr int kHeavyLog2 = 11;  // rows with >= 2048 neighbours
+
+template <typename T, typename RT, int SG, int R, int U>
+__global__ void __launch_bounds__(256) astep_heavy_kernel(AStepArgs A) {
+    constexpr int NG = 256 / SG;
+    constexpr int VN = Vec<T>::N;
+    constexpr int32_t kIdMask = (1 << kClassShift) - 1;
+    extern __shared__ __align__(16) unsigned char smem[];
+    __shared__ RT red[8];
+    T *sB = reinterpret_cast<T *>(smem);
+    uint4 *scratch = reinterpret_cast<uint4 *>(smem + ((A.smem_group * sizeof(T) + 15) / 16) * 16);
+    const int t = threadIdx.x, sg = t / SG, l = t % SG;
+    const int k = A.k;
+    const int64_t nvec_p = (A.ldseg_p > 0 ? A.ldseg_p : A.ldp) / VN;
+    const size_t row_bytes = (size_t)A.ldp * sizeof(T);
+    const uint64_t pol_last = policy_evict_last(), pol_first = A.hint ? policy_evict_first() : policy_evict_normal();
+    bool bad = false;
+    for (int64_t r = blockIdx.x; r < A.n; r += gridDim.x) {
+        int64_t iv[1];
+        bool actv[1] = {true};
+        const int64_t i = A.order[r];
+        iv[0] = i;
+        const int ci = A.colors[i];
+        for (int64_t q = t; q < A.ldb / VN; q += 256) reinterpret_cast<uint4 *>(sB)[q] = make_uint4(0, 0, 0, 0);
+        if (A.comb == COMB_GENERAL && A.stage_a && A.aoff != 0) {
+            const char *a = A.ma + (size_t)i * A.lda * sizeof(T);
+            for (int64_t q = t; q < A.lda / VN; q += 256) reinterpret_cast<uint4 *>(sB + A.ldb)[q] = ldg16(a + q * 16);
+        }
+        group_sync<256>(0);
+        const int32_t *h = A.hcnt + (size_t)i * A.kp;
+        int64_t e = A.rowptr[i];
+        for (int x = 0; x < k; ++x) {
+            const int cnt = __ldg(h + x);
+            if (x != ci && cnt > 0) {
+                const int rr = ci - (ci > x ? 1 : 0);
+                const int64_t sbase = A.ldseg_p > 0 ? (int64_t)rr * A.ldseg_p * (int64_t)sizeof(T) : 0;
+                uint4 acc[R];
+#pragma unroll
+                for (int q = 0; q < R; ++q) acc[q] = make_uint4(0, 0, 0, 0);
+                for (int c0 = sg; c0 < cnt; c0 += NG * U) {
+                    int32_t jj[U];
+                    uint64_t pol[U];
+#pragma unroll
+                    for (int u = 0; u < U; ++u) {
+                        const int c = c0 + u * NG;
+                        const int32_t b = c < cnt ? __ldg(A.bcol + e + c) : -1;
+                        jj[u] = (b >= 0 && A.tagged) ? (b & kIdMask) : b;
+                        pol[u] = (A.tagged && b >= 0 && (b >> kClassShift) < A.hot_log2) ? pol_last : pol_first;
+                    }
+                    uint4 xv[U][R];
+#pragma unroll
+                    for (int u = 0; u < U; ++u)
+#pragma unroll
+                        for (int q = 0; q < R; ++q) {
+                            const int64_t v = l + q * SG;
+                            xv[u][q] = ldg16_pred(A.mp + (size_t)(jj[u] >= 0 ? jj[u] : 0) * row_bytes + sbase + v * 16,
+                                                  jj[u] >= 0 && v < nvec_p, pol[u]);
+                        }
+#pragma unroll
+                    for (int u = 0; u < U; ++u)
+#pragma unroll
+                        for (int q = 0; q < R; ++q) Vec<T>::add(acc[q], xv[u][q]);
+                }
+#pragma unroll
+                for (int q = 0; q < R; ++q) scratch[(size_t)sg * SG * R + q * SG + l] = acc[q];
+                group_sync<256>(0);
+                // fixed-order sum of the NG partials, then push R_x into B (distinct targets)
+                const int32_t *mp = A.pmap + ((size_t)x * k + ci) * A.cp_map + A.u0;
+                for (int64_t v = t; v < nvec_p; v += 256) {
+                    const int q = (int)(v / SG), ll = (int)(v % SG);
+                    uint4 sum = scratch[q * SG + ll];
+                    for (int g2 = 1; g2 < NG; ++g2) Vec<T>::add(sum, scratch[(size_t)g2 * SG * R + q * SG + ll]);
+#pragma unroll
+                    for (int el = 0; el < VN; ++el) {
+                        const int64_t u = v * VN + el;
+                        if (u < A.cp) {
+                            const int32_t tt = __ldg(mp + u);
+                            if (tt >= 0) sB[tt] += vget<T>(sum, el);
+                        }
+                    }
+                }
+                group_sync<256>(0);
+            }
+            e += cnt;
+        }
+        ema_stage<T, RT, 256, 1>(A, sB, iv, actv, t, 0, red, bad);
+        group_sync<256>(0);
+    }
+    if (bad) atomicOr(A.ovf, 1);
+}
+
+template <typename T, typename RT, int SG, int R, int U>
+static int launch_astep_heavy_t(const AStepArgs &A, void *stream) {
+    constexpr int NG = 256 / SG;
+    const size_t smem = ((A.smem_group * sizeof(T) + 15) / 16) * 16 + (size_t)NG * SG * R * 16;
+    if (smem > 227 * 1024) return -1;
+    auto kern = astep_heavy_kernel<T, RT, SG, R, U>;
+    if (cudaError_t e = ensure_dyn_smem((const void *)kern, smem)) return (int)e;
+    int occ = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 256, smem);
+    if (occ < 1) occ = 1;
+    const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>(A.n, (int64_t)occ * num_sms()));
+    kern<<<(unsigned)blocks, 256, smem, (cudaStream_t)stream>>>(A);
+    return (int)cudaGetLastError();
+}
+
+// rows [0, A.n) of A.order are the heavy prefix; nvec = the gather row's 16-B vectors
+template <typename T, typename RT>
+static int launch_astep_heavy(const AStepArgs &A, int64_t nvec, void *stream) {
+    if (nvec <= 4) return launch_astep_heavy_t<T, RT, 4, 1, 4>(A, stream);
+    if (nvec <= 8) return launch_astep_heavy_t<T, RT, 8, 1, 4>(A, stream);
+    if (nvec <= 16) return launch_astep_heavy_t<T, RT, 16, 1, 4>(A, stream);
+    if (nvec <= 32) return launch_astep_heavy_t<T, RT, 16, 2, 4>(A, stream);
+    if (nvec <= 64) return launch_astep_heavy_t<T, RT, 16, 4, 2>(A, stream);
+    return launch_astep_heavy_t<T, RT, 16, 8, 1>(A, stream);
+}
+
+// ---------------------------------------------------------------------------
 // bulk-staged fused step (wide rows): the gather of stage 1 is fed by the TMA engine.
 // One producer warp walks the neighbour list of the CTA's rows in colour-bucket order
 // (the row's own colour skipped) and issues one cp.async.bulk per neighbour — its whole
@@ -669,17 +797,18 @@ __global__ void __launch_bounds__(kBulkThreads, 3) astep_bulk_kernel(AStepArgs A
 // ---------------------------------------------------------------------------
 // top step, leaf active child: colorful_i = Σ_{j∈N(i), c(j)≠c(i)} M_p(j, topcol[c(j)][c(i)])
 // ---------------------------------------------------------------------------
+// colors: indexed by global vertex id (neighbours); row i's own colour is colors[row_begin + i]
 template <typename T, typename RT>
 __global__ void __launch_bounds__(256) atop_leaf_kernel(int64_t n, int k, int kp, const int64_t *__restrict__ rowptr,
                                                         const int32_t *__restrict__ col,
                                                         const uint8_t *__restrict__ colors,
                                                         const int32_t *__restrict__ hcnt, const T *__restrict__ src,
                                                         int64_t ldp, int src_hist, const int32_t *__restrict__ topcol,
-                                                        RT *__restrict__ rowval) {
+                                                        RT *__restrict__ rowval, int64_t row_begin) {
     const int lane = threadIdx.x & 31;
     const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
     for (int64_t i = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); i < n; i += warps) {
-        const int ci = colors[i];
+        const int ci = colors[row_begin + i];
         RT acc = 0;
         if (src_hist) {  // k = 2: the one other colour
             if (lane == 0) acc = (RT)hcnt[(size_t)i * kp + (ci == 0 ? 1 : 0)];
@@ -824,13 +953,26 @@ static int launch_astep_cfg(const AStepArgs &A0, void *stream) {
         const char *e = getenv("SG2V_BULK");
         bulk = e ? atoi(e) : 1;
         const char *m = getenv("SG2V_BULK_MIN");
-        bulk_min = m ? atoi(m) : 64;
+        bulk_min = m ? atoi(m) : 128;
     }
     if (MODE == 0 && bulk && !multi && !A.src_hist && A.pmap != nullptr && nvec >= bulk_min && nvec <= 2048) {
         if (nvec <= 256) return launch_astep_bulk_t<T, RT, 1>(A, stream);
         if (nvec <= 512) return launch_astep_bulk_t<T, RT, 2>(A, stream);
         if (nvec <= 1024) return launch_astep_bulk_t<T, RT, 4>(A, stream);
         return launch_astep_bulk_t<T, RT, 8>(A, stream);
+    }
+    // heavy rows of narrow register-gather steps: CTA per row first, the rest after
+    // (SG2V_HEAVY=0 disables)
+    static int heavy = -1;
+    if (heavy < 0) { const char *e = getenv("SG2V_HEAVY"); heavy = e ? atoi(e) : 1; }
+    if (MODE == 0 && heavy && !multi && !A.src_hist && A.pmap != nullptr && gt < 256 && nvec <= 128 &&
+        A.n_heavy > 0 && A.n_heavy < A.n) {
+        AStepArgs H = A;
+        H.n = A.n_heavy;
+        int rc = launch_astep_heavy<T, RT>(H, nvec, stream);
+        if (rc) return rc;
+        A.order += A.n_heavy;
+        A.n -= A.n_heavy;
     }
     if constexpr (MODE != 0) {
         if constexpr (MODE == 2) {
@@ -879,23 +1021,26 @@ int launch_astep_vp(const Graph &g, const Plan &pl, const Step &st, const uint8_
                     const int32_t *bcol, char *tables, void *rowval, int *ovf, void *stream, const VpArgs *vp) {
     if (g.n <= 0) return 0;
     const int32_t *idx = pl.d_index + st.idx_off;
-    const char *src = (st.src == SRC_HIST || (vp && vp->mode == 2)) ? nullptr : tables + pl.bufs[st.buf_p].offset;
-    if (st.top && st.comb == COMB_ACTIVE_LEAF && !vp) {
+    const char *src = (st.src == SRC_HIST || (vp && vp->mode == 2)) ? nullptr
+                      : (vp && vp->mode == 3) ? vp->stage : tables + pl.bufs[st.buf_p].offset;
+    // vertex mode, whole rows: neighbour ids are global, this rank's rows start at row_begin
+    const int64_t colour_off = (vp && vp->mode == 3) ? vp->row_begin : 0;
+    if (st.top && st.comb == COMB_ACTIVE_LEAF && (!vp || vp->mode == 3)) {
         int64_t blocks = std::min<int64_t>((g.n + 7) / 8, (int64_t)num_sms() * 8);
         int srch = st.src == SRC_HIST;
         prof_begin(3, stream);
         if (pl.prec == SG2V_F32)
             atop_leaf_kernel<float, double><<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(
-                g.n, pl.k, (int)pl.kp, g.d_rowptr, g.d_col, colors, hcnt, (const float *)src, st.ldp, srch, idx,
-                (double *)rowval);
+                g.n, pl.k, (int)pl.kp, g.d_rowptr, g.d_col, colors - colour_off, hcnt, (const float *)src, st.ldp, srch, idx,
+                (double *)rowval, colour_off);
         else if (pl.prec == SG2V_F64)
             atop_leaf_kernel<double, double><<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(
-                g.n, pl.k, (int)pl.kp, g.d_rowptr, g.d_col, colors, hcnt, (const double *)src, st.ldp, srch, idx,
-                (double *)rowval);
+                g.n, pl.k, (int)pl.kp, g.d_rowptr, g.d_col, colors - colour_off, hcnt, (const double *)src, st.ldp, srch, idx,
+                (double *)rowval, colour_off);
         else
             atop_leaf_kernel<u64, u64><<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(
-                g.n, pl.k, (int)pl.kp, g.d_rowptr, g.d_col, colors, hcnt, (const u64 *)src, st.ldp, srch, idx,
-                (u64 *)rowval);
+                g.n, pl.k, (int)pl.kp, g.d_rowptr, g.d_col, colors - colour_off, hcnt, (const u64 *)src, st.ldp, srch, idx,
+                (u64 *)rowval, colour_off);
         prof_end(3, st.alg_bytes, stream, st.impl_bytes, 0.0);
         return (int)cudaGetLastError();
     }
@@ -939,6 +1084,7 @@ int launch_astep_vp(const Graph &g, const Plan &pl, const Step &st, const uint8_
     A.bsrc_global = 0;
     A.bg = nullptr;
     A.ovf = ovf;
+    A.n_heavy = g.n_deg_ge[kHeavyLog2];
     // stage M_a next to B only while both fit comfortably (occupancy); else L1
     A.aoff = st.self_a ? 0 : st.ldb;
     static int stage_kb = -1;  // SG2V_STAGE_KB (experiments): M_a staging threshold
@@ -981,11 +1127,13 @@ int launch_astep_vp(const Graph &g, const Plan &pl, const Step &st, const uint8_
         A.bsrc_global = 1;
         A.bg = vp->bg;
         A.src_hist = 0;
+    } else if (vp && vp->mode == 3) {  // fused step, whole rows from the staging buffer
+        A.hint = 0;
     }
     int cls = st.top ? 3 : 2;
     prof_begin(cls, stream);
     int rc;
-    const int md = vp ? vp->mode : 0;
+    const int md = vp && vp->mode != 3 ? vp->mode : 0;
     if (pl.prec == SG2V_F32)
         rc = md == 1 ? launch_astep_cfg<float, double, 1>(A, stream)
                      : md == 2 ? launch_astep_cfg<float, double, 2>(A, stream) : launch_astep_cfg<float, double, 0>(A, stream);
@@ -996,9 +1144,10 @@ int launch_astep_vp(const Graph &g, const Plan &pl, const Step &st, const uint8_
         rc = md == 1 ? launch_astep_cfg<u64, u64, 1>(A, stream)
                      : md == 2 ? launch_astep_cfg<u64, u64, 2>(A, stream) : launch_astep_cfg<u64, u64, 0>(A, stream);
     // algorithmic bytes of a column tile: its share of the step's gather
-    const double tile_frac = !vp ? 1.0 : (vp->mode == 1 ? (double)vp->cnt / (double)std::max<int64_t>(st.cp, 1) : 0.0);
+    const double tile_frac = (!vp || vp->mode == 3) ? 1.0
+                             : (vp->mode == 1 ? (double)vp->cnt / (double)std::max<int64_t>(st.cp, 1) : 0.0);
     prof_end(cls, st.alg_bytes * tile_frac, stream, st.impl_bytes * tile_frac,
-             !vp || vp->mode == 2 ? st.ema_terms : 0.0);
+             !vp || vp->mode >= 2 ? st.ema_terms : 0.0);
     return rc;
 }
 

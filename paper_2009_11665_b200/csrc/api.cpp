@@ -310,6 +310,7 @@ void sg2v_graph_free(sg2v_graph *g) {
     if (g->d_col) cudaFreeAsync(g->d_col, 0);
     if (g->d_order) cudaFreeAsync(g->d_order, 0);
     if (g->d_vclass) cudaFreeAsync(g->d_vclass, 0);
+    if (g->d_orig) cudaFreeAsync(g->d_orig, 0);
     cudaSetDevice(cur);
     delete g;
 }
@@ -548,10 +549,28 @@ static sg2v_status comm_allgather(sg2v_comm *c, const void *send, void *recv, si
 }
 
 // 1D vertex partition: rank r owns rows [r·nl, r·nl + n_local) of
-// every table (nl = ceil(n_global / world)); per gather step the passive table is
-// all-gathered column tile by column tile into [world·nl][tile_w] staging and each
-// rank pushes its own rows' colour-bucket sums into B rows in global memory; the
-// eMA / top then run on the local rows, and the per-rank Σ_i are all-gathered.
+// every table (nl = ceil(n_global / world)).  Per gather step the passive table is
+// exchanged either as whole rows (plan vp_full: one all-gather of every rank's table
+// — its table holds nl rows, so it is the send buffer — then the fused single-GPU
+// kernels run on the local rows with the staging buffer as the gather source; nothing
+// is exchanged at world = 1), or, for passive tables too large to stage, in column
+// tiles: pack + all-gather of tile t+1 run on a communication stream while the push
+// of tile t's colour-bucket sums into B rows in global memory runs on the compute
+// stream (double-buffered staging, events order both ways); the eMA / top then run on
+// the local rows.  The per-rank Σ_i are all-gathered and summed in rank order.
+struct VpStreams {
+    cudaStream_t comm = nullptr;
+    cudaEvent_t ready[2] = {nullptr, nullptr}, done[2] = {nullptr, nullptr}, src = nullptr;
+    ~VpStreams() {
+        for (int q = 0; q < 2; ++q) {
+            if (ready[q]) cudaEventDestroy(ready[q]);
+            if (done[q]) cudaEventDestroy(done[q]);
+        }
+        if (src) cudaEventDestroy(src);
+        if (comm) cudaStreamDestroy(comm);
+    }
+};
+
 static sg2v_status count_vp(const sg2v_graph *g, const sg2v_template *t, int32_t k, int64_t n_iter, uint64_t seed,
                             sg2v_options o, double *estimate, double *colorful_out, uint64_t *colorful_u64_out) {
     sg2v_comm *c = (sg2v_comm *)o.nccl_comm;
@@ -578,15 +597,16 @@ static sg2v_status count_vp(const sg2v_graph *g, const sg2v_template *t, int32_t
     if (k == 1) {
         for (int64_t q = 0; q < n_iter; ++q) { resf[q] = (double)n_global; resu[q] = (uint64_t)n_global; }
     } else {
-        // plan on the local rows; staging sized for world·nl global rows
-        auto key = std::make_tuple((int)o.precision, g->n, g->nnz, -(g->device + 1) - 1000 * c->world, 0,
+        // plan on nl rows (every rank's tables hold nl rows: the whole-row exchange sends
+        // them as they are); staging sized for world·nl global rows
+        auto key = std::make_tuple((int)o.precision, nl, g->nnz, -(g->device + 1) - 1000 * c->world, 0,
                                    (uint64_t)o.col_tile, (int64_t)c->world * nl);
         Template &tm = const_cast<Template &>(*(const Template *)t);
         std::unique_lock<std::mutex> plan_lock(tm.mu);
         auto &slot = tm.plans[key];
         if (!slot) {
             std::unique_ptr<Plan> pl;
-            st = make_plan(*t, std::max<int64_t>(g->n, 1), std::max<int64_t>(g->nnz, 1), o.precision, LAYOUT_ANCHORED,
+            st = make_plan(*t, std::max<int64_t>(nl, 1), std::max<int64_t>(g->nnz, 1), o.precision, LAYOUT_ANCHORED,
                            0, pl, (int64_t)c->world * nl, o.col_tile, 0);
             if (st != SG2V_OK) return st;
             slot = std::move(pl);
@@ -610,6 +630,15 @@ static sg2v_status count_vp(const sg2v_graph *g, const sg2v_template *t, int32_t
             own = true;
         }
         struct Free { char *p; bool own; cudaStream_t s; ~Free() { if (own) cudaFreeAsync(p, s); } } freer{ws, own, s};
+        VpStreams vs;
+        if (!pl->vp_full) {
+            SG2V_CK(cudaStreamCreateWithFlags(&vs.comm, cudaStreamNonBlocking));
+            for (int q = 0; q < 2; ++q) {
+                SG2V_CK(cudaEventCreateWithFlags(&vs.ready[q], cudaEventDisableTiming));
+                SG2V_CK(cudaEventCreateWithFlags(&vs.done[q], cudaEventDisableTiming));
+            }
+            SG2V_CK(cudaEventCreateWithFlags(&vs.src, cudaEventDisableTiming));
+        }
         uint8_t *colors_g = (uint8_t *)(ws + pl->off_colors_g);
         uint8_t *colors_l = colors_g + begin;
         int32_t *hcnt = (int32_t *)(ws + pl->off_hcnt);
@@ -622,42 +651,81 @@ static sg2v_status count_vp(const sg2v_graph *g, const sg2v_template *t, int32_t
         const int64_t E = pl->elem, W = pl->tile_w;
         const int vn = 16 / pl->elem;
         std::vector<uint64_t> hpart(c->world);
+        int fill = 0;  // tile ordinal (staging parity) across steps
         for (int64_t q = 0; q < n_iter; ++q) {
             const int64_t j = o.iter_offset + q * o.iter_stride;
-            int rc = launch_colorize(seed, j, n_global, k, colors_g, s);  // every rank colours every vertex
+            // every rank colours every vertex (a pure function of its input id)
+            int rc = launch_colorize(seed, j, n_global, k, colors_g, s, g->d_orig);
             if (rc) return cuda_fail("colorize", rc);
             if (g->n > 0 && (rc = launch_bucket(*g, *pl, colors_g, hcnt, bcol, s))) return cuda_fail("bucket", rc);
-            int par = 0;
             for (const Step &stp : pl->steps) {
                 if (stp.src == SRC_HIST) {  // local (the histogram is local)
                     rc = launch_astep_vp(*g, *pl, stp, colors_l, hcnt, bcol, ws, rowval, dflag, s, nullptr);
                     if (rc) return cuda_fail("step", rc == -1 ? 0 : rc);
                     continue;
                 }
+                const char *mp = ws + pl->bufs[stp.buf_p].offset;
+                if (pl->vp_full) {
+                    // whole rows: one all-gather of the passive table (nl rows per rank)
+                    const char *stage = mp;
+                    if (c->world > 1) {
+                        st = comm_allgather(c, mp, ws + pl->off_stage, (size_t)nl * stp.ldp * E, s);
+                        if (st != SG2V_OK) return st;
+                        stage = ws + pl->off_stage;
+                    }
+                    VpArgs va;
+                    va.mode = 3;
+                    va.stage = stage;
+                    va.row_begin = begin;
+                    rc = launch_astep_vp(*g, *pl, stp, colors_l, hcnt, bcol, ws, rowval, dflag, s, &va);
+                    if (rc) return cuda_fail("step", rc == -1 ? 0 : rc);
+                    continue;
+                }
                 const bool bg_is_out = !stp.top && stp.comb == COMB_ACTIVE_LEAF;
                 char *bg = bg_is_out ? ws + pl->bufs[stp.buf_out].offset : ws + pl->off_bg;
                 SG2V_CK(cudaMemsetAsync(bg, 0, (size_t)std::max<int64_t>(g->n, 1) * stp.ldb * E, s));
-                const char *mp = ws + pl->bufs[stp.buf_p].offset;
-                for (int64_t u0 = 0; u0 < stp.cp; u0 += W) {
+                // the comm stream packs the passive table written by the previous step
+                SG2V_CK(cudaEventRecord(vs.src, s));
+                SG2V_CK(cudaStreamWaitEvent(vs.comm, vs.src, 0));
+                auto exchange = [&](int64_t u0, int par) -> sg2v_status {
                     const int64_t cnt = std::min<int64_t>(W, stp.cp - u0);
                     const int64_t wb = ((cnt + vn - 1) / vn) * vn * E;
                     char *send = ws + pl->off_send + (size_t)par * nl * W * E;
                     char *stage = ws + pl->off_stage + (size_t)par * c->world * nl * W * E;
-                    if (g->n > 0 && (rc = launch_pack_tile(g->n, mp, stp.ldp * E, u0 * E, wb, send, W * E, s)))
-                        return cuda_fail("pack", rc);
-                    st = comm_allgather(c, send, stage, (size_t)nl * W * E, s);
-                    if (st != SG2V_OK) return st;
+                    int r2 = g->n > 0 ? launch_pack_tile(g->n, mp, stp.ldp * E, u0 * E, wb, send, W * E, vs.comm) : 0;
+                    if (r2) return cuda_fail("pack", r2);
+                    sg2v_status s2 = comm_allgather(c, send, stage, (size_t)nl * W * E, vs.comm);
+                    if (s2 != SG2V_OK) return s2;
+                    SG2V_CK(cudaEventRecord(vs.ready[par], vs.comm));
+                    return SG2V_OK;
+                };
+                const int64_t ntiles = (stp.cp + W - 1) / W;
+                // prologue: tile 0 in flight
+                if ((st = exchange(0, fill & 1)) != SG2V_OK) return st;
+                for (int64_t tt = 0; tt < ntiles; ++tt) {
+                    const int par = (fill + (int)tt) & 1;
+                    // next tile's exchange overlaps this tile's push (its staging half
+                    // was last read by tile tt-1: wait for that push first)
+                    if (tt + 1 < ntiles) {
+                        if (tt >= 1) SG2V_CK(cudaStreamWaitEvent(vs.comm, vs.done[par ^ 1], 0));
+                        if ((st = exchange((tt + 1) * W, par ^ 1)) != SG2V_OK) return st;
+                    }
+                    SG2V_CK(cudaStreamWaitEvent(s, vs.ready[par], 0));
                     VpArgs va;
                     va.mode = 1;
-                    va.stage = stage;
+                    va.stage = ws + pl->off_stage + (size_t)par * c->world * nl * W * E;
                     va.stage_ld = W;
-                    va.u0 = u0;
-                    va.cnt = cnt;
+                    va.u0 = tt * W;
+                    va.cnt = std::min<int64_t>(W, stp.cp - tt * W);
                     va.bg = bg;
                     rc = launch_astep_vp(*g, *pl, stp, colors_l, hcnt, bcol, ws, rowval, dflag, s, &va);
                     if (rc) return cuda_fail("tile", rc == -1 ? 0 : rc);
-                    par ^= 1;
+                    SG2V_CK(cudaEventRecord(vs.done[par], s));
                 }
+                fill += (int)ntiles;
+                // the comm stream must not run ahead into buffers of the next step
+                SG2V_CK(cudaEventRecord(vs.src, s));
+                SG2V_CK(cudaStreamWaitEvent(vs.comm, vs.src, 0));
                 if (bg_is_out) continue;
                 if (stp.top && stp.comb == COMB_ACTIVE_LEAF) {
                     rc = launch_bg_rowval(*pl, g->n, bg, stp.ldb, rowval, s);
@@ -690,6 +758,7 @@ static sg2v_status count_vp(const sg2v_graph *g, const sg2v_template *t, int32_t
             resu[q] = su;
             resf[q] = sf;
         }
+        if (vs.comm) SG2V_CK(cudaStreamSynchronize(vs.comm));
         if (!u64mode) SG2V_CK((cudaError_t)ovf_read(dflag, &ovf, s));
     }
     bool finite = ovf == 0;  // a stored F32 table entry overflowed on this rank
@@ -802,7 +871,7 @@ static sg2v_status count_core(const sg2v_graph *g, const sg2v_template *const *t
         if (!u64mode) SG2V_CK((cudaError_t)ovf_reset(dflag, s));
         for (int64_t q = 0; q < n_iter; ++q) {
             const int64_t j = o.iter_offset + q * o.iter_stride;
-            int rc = launch_colorize(seed, j, g->n, k, colors, s);
+            int rc = launch_colorize(seed, j, g->n, k, colors, s, g->d_orig);
             if (rc) return cuda_fail("colorize", rc);
             if (need_hist && (rc = launch_hist(*g, *pls[0], colors, H, s))) return cuda_fail("hist", rc);
             if (anch && (rc = launch_bucket(*g, *pls[0], colors, hcnt, bcol, s))) return cuda_fail("bucket", rc);
@@ -974,6 +1043,70 @@ sg2v_status sg2v_graph_load_partition(int64_t n_global, int64_t row_begin, int64
     (*out)->partitioned = true;
     (*out)->n_global = n_global;
     (*out)->row_begin = row_begin;
+    return SG2V_OK;
+}
+
+sg2v_status sg2v_graph_set_vertex_ids(sg2v_graph *g, const int32_t *orig_ids, int64_t count) {
+    if (!g || (count > 0 && !orig_ids)) { set_error("NULL argument"); return SG2V_EINVAL; }
+    const int64_t want = g->partitioned ? g->n_global : g->n;
+    if (count != want) { set_error("count must be n (n_global for a partition)"); return SG2V_EINVAL; }
+    for (int64_t v = 0; v < count; ++v)
+        if (orig_ids[v] < 0) { set_error("vertex ids must be non-negative"); return SG2V_EINVAL; }
+    int cur = 0;
+    cudaGetDevice(&cur);
+    cudaSetDevice(g->device);
+    struct Restore { int d; ~Restore() { cudaSetDevice(d); } } restore{cur};
+    if (g->d_orig) { cudaFree(g->d_orig); g->d_orig = nullptr; }
+    if (count == 0) return SG2V_OK;
+    SG2V_CK(cudaMalloc((void **)&g->d_orig, count * sizeof(int32_t)));
+    SG2V_CK(cudaMemcpy(g->d_orig, orig_ids, count * sizeof(int32_t), cudaMemcpyHostToDevice));
+    return SG2V_OK;
+}
+
+sg2v_status sg2v_partition_relabel(int64_t n, const int64_t *row_offsets, const int32_t *col_indices, int32_t world,
+                                   int32_t *old_of_new, int64_t *ro_out, int32_t *ci_out) {
+    if (n < 0 || world < 1 || !row_offsets || !old_of_new || !ro_out || (row_offsets[n] > 0 && (!col_indices || !ci_out))) {
+        set_error("bad argument");
+        return SG2V_EINVAL;
+    }
+    // blocks of nl consecutive new ids (the last one shorter); vertices dealt by degree,
+    // heaviest first, in snake order over the blocks that still have room, so every block
+    // gets a near-equal share of the edges (nnz) as well as of the rows
+    const int64_t nl = (n + world - 1) / world;
+    std::vector<int64_t> cap(world), fill(world, 0);
+    for (int r = 0; r < world; ++r) cap[r] = std::max<int64_t>(0, std::min(nl, n - (int64_t)r * nl));
+    std::vector<int32_t> by_deg(n);
+    for (int64_t v = 0; v < n; ++v) by_deg[v] = (int32_t)v;
+    std::stable_sort(by_deg.begin(), by_deg.end(), [&](int32_t a, int32_t b) {
+        return row_offsets[a + 1] - row_offsets[a] > row_offsets[b + 1] - row_offsets[b];
+    });
+    std::vector<int32_t> new_of_old(n);
+    int r = 0, dir = 1;
+    for (int64_t q = 0; q < n; ++q) {
+        int guard = 0;
+        while (fill[r] >= cap[r] && guard++ < 2 * world) {  // skip full blocks
+            r += dir;
+            if (r == world) { r = world - 1; dir = -1; }
+            if (r < 0) { r = 0; dir = 1; }
+        }
+        const int32_t v = by_deg[q];
+        const int64_t id = (int64_t)r * nl + fill[r]++;
+        new_of_old[v] = (int32_t)id;
+        old_of_new[id] = v;
+        r += dir;
+        if (r == world) { r = world - 1; dir = -1; }
+        if (r < 0) { r = 0; dir = 1; }
+    }
+    // relabelled CSR: row u = old row old_of_new[u], columns mapped and sorted
+    ro_out[0] = 0;
+    for (int64_t u = 0; u < n; ++u) {
+        const int32_t v = old_of_new[u];
+        const int64_t d = row_offsets[v + 1] - row_offsets[v];
+        ro_out[u + 1] = ro_out[u] + d;
+        int32_t *dst = ci_out + ro_out[u];
+        for (int64_t e = 0; e < d; ++e) dst[e] = new_of_old[col_indices[row_offsets[v] + e]];
+        std::sort(dst, dst + d);
+    }
     return SG2V_OK;
 }
 

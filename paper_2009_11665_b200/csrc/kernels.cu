@@ -38,10 +38,13 @@ __device__ __forceinline__ u64 mix64(u64 z) {
     return z;
 }
 
-__global__ void colorize_kernel(u64 seed, int64_t j, int64_t n, int k, uint8_t *__restrict__ out) {
+// ids (optional): vertex v is input vertex ids[v] (relabelled graphs colour by input id)
+__global__ void colorize_kernel(u64 seed, int64_t j, int64_t n, int k, uint8_t *__restrict__ out,
+                                const int32_t *__restrict__ ids) {
     const u64 key = mix64(seed + 0x9E3779B97F4A7C15ULL * (u64)(j + 1));
     for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n; v += (int64_t)gridDim.x * blockDim.x) {
-        u64 h = mix64(key ^ ((u64)v * 0xD6E8FEB86659FD93ULL));
+        const u64 id = ids ? (u64)(uint32_t)ids[v] : (u64)v;
+        u64 h = mix64(key ^ (id * 0xD6E8FEB86659FD93ULL));
         out[v] = (uint8_t)(((h >> 32) * (u64)k) >> 32);
     }
 }
@@ -285,6 +288,19 @@ __global__ void degree_kernel(int64_t n, const int64_t *__restrict__ rowptr, int
     }
 }
 
+// cnt[q] = number of rows with degree >= 2^q in the descending degree array
+__global__ void deg_count_kernel(const int32_t *__restrict__ deg_sorted, int64_t n, int64_t *__restrict__ cnt) {
+    const int q = threadIdx.x;
+    if (q >= 32) return;
+    const int64_t thr = int64_t(1) << q;
+    int64_t lo = 0, hi = n;  // first position with degree < thr
+    while (lo < hi) {
+        const int64_t mid = (lo + hi) / 2;
+        if ((int64_t)deg_sorted[mid] >= thr) lo = mid + 1; else hi = mid;
+    }
+    cnt[q] = lo;
+}
+
 __global__ void vclass_kernel(int64_t n, const int32_t *__restrict__ order, uint8_t *__restrict__ vclass) {
     for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n; r += (int64_t)gridDim.x * blockDim.x)
         vclass[order[r]] = (uint8_t)(63 - __clzll((unsigned long long)(r + 1)));
@@ -328,11 +344,11 @@ int num_sms() {
     return sms;
 }
 
-int launch_colorize(uint64_t seed, int64_t j, int64_t n, int k, uint8_t *out, void *stream) {
+int launch_colorize(uint64_t seed, int64_t j, int64_t n, int k, uint8_t *out, void *stream, const int32_t *ids) {
     if (n <= 0) return 0;
     int64_t blocks = std::min<int64_t>((n + 255) / 256, (int64_t)num_sms() * 16);
     prof_begin(0, stream);
-    colorize_kernel<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(seed, j, n, k, out);
+    colorize_kernel<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(seed, j, n, k, out, ids);
     prof_end(0, (double)n, stream);
     return (int)cudaGetLastError();
 }
@@ -469,6 +485,14 @@ int graph_build_order(Graph &g, void *stream) {
         cudaFreeAsync(tmp, s);
         e = cudaStreamSynchronize(s);
         g.max_deg = mx;
+        // rows with degree >= 2^q (a prefix of the descending order), one thread per q
+        int64_t *d_cnt = nullptr;
+        if (e == cudaSuccess && (e = cudaMallocAsync((void **)&d_cnt, 32 * sizeof(int64_t), s)) == cudaSuccess) {
+            deg_count_kernel<<<1, 32, 0, s>>>(deg_sorted, n, d_cnt);
+            cudaMemcpyAsync(g.n_deg_ge, d_cnt, 32 * sizeof(int64_t), cudaMemcpyDeviceToHost, s);
+            cudaFreeAsync(d_cnt, s);
+            e = cudaStreamSynchronize(s);
+        }
     }
     cudaFreeAsync(deg, s);
     if (e != cudaSuccess) return (int)e;

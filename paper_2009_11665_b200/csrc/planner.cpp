@@ -641,7 +641,7 @@ static bool build_index(Plan &pl) {
                         }
                 push_maps_x[st.p] = st.map_off;
             }
-        } else if (anch && st.src == SRC_GATHER && (pl.vp || !(st.top && st.comb == COMB_ACTIVE_LEAF))) {
+        } else if (anch && st.src == SRC_GATHER && ((pl.vp && !pl.vp_full) || !(st.top && st.comb == COMB_ACTIVE_LEAF))) {
             auto it = push_maps.find(st.p);
             if (it != push_maps.end()) {
                 st.map_off = it->second;
@@ -668,7 +668,7 @@ static bool build_index(Plan &pl) {
         }
         align();
         st.idx_off = (int64_t)pl.index.size();
-        if (st.top && st.comb == COMB_ACTIVE_LEAF && pl.vp) {
+        if (st.top && st.comb == COMB_ACTIVE_LEAF && pl.vp && !pl.vp_full) {
             pl.index.push_back(0);  // vertex-partitioned: colorful_i = B(i, [k-1]) from bg (push map above)
         } else if (st.top && st.comb == COMB_ACTIVE_LEAF) {
             if (!anch) {
@@ -751,25 +751,39 @@ static bool build_index(Plan &pl) {
 // tile_w elements into a [n_global][tile_w] staging buffer (double buffered), and
 // pushes into B rows in global memory (bg; the output table itself for
 // leaf-active steps).
+// Full-row exchange (vp_full): when the widest passive table of all ranks fits the
+// staging cap, each gather step all-gathers whole rows (every rank's table holds nl
+// rows, so its table IS the send buffer) and runs the fused single-GPU kernels on the
+// local rows with the staging buffer as the gather source (B stays on chip); at
+// world = 1 nothing is exchanged at all.  Otherwise column tiles as above.
 static void plan_vp_extend(Plan &pl, int64_t n_local, int64_t n_global, int64_t tile_req) {
     const int vn = 16 / pl.elem;
-    int64_t max_cp = 0, max_bg = 0;
+    int64_t max_cp = 0, max_bg = 0, max_ldp = 0;
     for (Step &st : pl.steps) {
         if (st.src != SRC_GATHER) continue;
         max_cp = std::max(max_cp, round_up(st.cp, vn));
+        max_ldp = std::max(max_ldp, st.ldp);
         const bool bg_is_out = !st.top && st.comb == COMB_ACTIVE_LEAF;
         if (!bg_is_out) max_bg = std::max(max_bg, st.ldb);
     }
-    int64_t w = tile_req > 0 ? round_up(tile_req, vn)
-                             : std::max<int64_t>(vn, ((2048ll << 20) / std::max<int64_t>(n_global * pl.elem, 1)) / vn * vn);
-    w = std::max<int64_t>(vn, std::min(w, std::max<int64_t>(max_cp, vn)));
+    static const int64_t kFullCap = 24ll << 30;  // staging bytes allowed for full rows
     pl.n_global = n_global;
-    pl.tile_w = w;
+    pl.vp_full = tile_req <= 0 && n_global * max_ldp * pl.elem <= kFullCap;
     int64_t off = pl.ws_bytes;
     pl.off_colors_g = off; off = round_up(off + std::max<int64_t>(n_global, 1) + 16, 256);
-    pl.off_stage = off;    off = round_up(off + 2 * n_global * w * pl.elem, 256);
-    pl.off_send = off;     off = round_up(off + 2 * std::max<int64_t>(n_local, 1) * w * pl.elem, 256);
-    pl.off_bg = off;       off = round_up(off + std::max<int64_t>(n_local, 1) * max_bg * pl.elem, 256);
+    if (pl.vp_full) {
+        pl.tile_w = max_ldp;
+        pl.off_stage = off;  off = round_up(off + (n_global > n_local ? n_global * max_ldp * pl.elem : 0), 256);
+        pl.off_send = pl.off_bg = off;
+    } else {
+        int64_t w = tile_req > 0 ? round_up(tile_req, vn)
+                                 : std::max<int64_t>(vn, ((2048ll << 20) / std::max<int64_t>(n_global * pl.elem, 1)) / vn * vn);
+        w = std::max<int64_t>(vn, std::min(w, std::max<int64_t>(max_cp, vn)));
+        pl.tile_w = w;
+        pl.off_stage = off;  off = round_up(off + 2 * n_global * w * pl.elem, 256);
+        pl.off_send = off;   off = round_up(off + 2 * std::max<int64_t>(n_local, 1) * w * pl.elem, 256);
+        pl.off_bg = off;     off = round_up(off + std::max<int64_t>(n_local, 1) * max_bg * pl.elem, 256);
+    }
     pl.off_part = off;     off = round_up(off + 4096 * 8, 256);
     pl.ws_bytes = off;
 }

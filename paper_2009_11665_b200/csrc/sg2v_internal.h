@@ -29,18 +29,25 @@ struct Graph {
     int32_t *d_order = nullptr;  // rows sorted by degree, descending
     uint8_t *d_vclass = nullptr; // floor(log2(1 + rank in degree order)) per vertex (L2 hints)
     int64_t max_deg = 0;
+    int64_t n_deg_ge[32] = {0};  // rows with degree >= 2^q (a prefix of d_order)
     // vertex-partitioned mode: this handle holds rows
     // [row_begin, row_begin + n) of a graph with n_global vertices; col ids are global
     bool partitioned = false;
     int64_t n_global = 0, row_begin = 0;
+    // optional relabelling (sg2v_graph_set_vertex_ids): vertex v of this graph is vertex
+    // d_orig[v] of the caller's input graph; colours are keyed by that id (SURVEY §8(c)
+    // "RNG": reordering must carry original ids).  n_global entries when partitioned.
+    int32_t *d_orig = nullptr;
 };
 
 // Column tile / combine descriptor of a vertex-partitioned step.
 struct VpArgs {
-    int mode = 0;               // 1 = tile gather into bg, 2 = combine from bg
+    int mode = 0;               // 1 = tile gather into bg, 2 = combine from bg,
+                                // 3 = fused step gathering whole rows from `stage`
     const char *stage = nullptr;  // [n_global][stage_ld] all-gathered column tile
     int64_t stage_ld = 0, u0 = 0, cnt = 0;
     char *bg = nullptr;         // [n_local][ldb]
+    int64_t row_begin = 0;      // mode 3: first global row of this rank
 };
 
 // ---------------------------------------------------------------------------
@@ -109,6 +116,7 @@ struct Plan {
     int64_t off_hcnt = 0, off_bcol = 0;   // anchored: colour counts + colour-bucketed CSR
     // vertex-partitioned mode: rows are local (n = n_local), colours/staging are global
     bool vp = false;
+    bool vp_full = false;                  // whole passive rows exchanged (no column tiles)
     int64_t n_global = 0, tile_w = 0;      // tile width in elements (multiple of 16 B)
     int64_t off_stage = 0, off_send = 0, off_bg = 0, off_colors_g = 0, off_part = 0;
     int64_t ws_bytes = 0;
@@ -153,7 +161,8 @@ int64_t binom(int n, int r);
 
 // kernels.cu — launchers; all return cudaError_t as int (0 = success)
 struct Profiler;
-int launch_colorize(uint64_t seed, int64_t j, int64_t n, int k, uint8_t *out, void *stream);
+int launch_colorize(uint64_t seed, int64_t j, int64_t n, int k, uint8_t *out, void *stream,
+                    const int32_t *ids = nullptr);
 int launch_hist(const Graph &g, const Plan &pl, const uint8_t *colors, void *H, void *stream);
 int launch_bucket(const Graph &g, const Plan &pl, const uint8_t *colors, int32_t *hcnt, int32_t *bcol,
                   void *stream);

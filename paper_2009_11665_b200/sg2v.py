@@ -56,7 +56,7 @@ SYMBOLS = ["sg2v_graph_load_csr", "sg2v_graph_free", "sg2v_template_build", "sg2
            "sg2v_profile_read", "sg2v_last_error", "sg2v_version", "sg2v_count_batch",
            "sg2v_workspace_bytes_batch", "sg2v_comm_unique_id", "sg2v_comm_init_nccl", "sg2v_comm_init_callback",
            "sg2v_comm_free", "sg2v_graph_load_partition", "sg2v_estimate",
-           "sg2v_profile_read_launches"]
+           "sg2v_profile_read_launches", "sg2v_partition_relabel", "sg2v_graph_set_vertex_ids"]
 
 ALLGATHER_FN = ctypes.CFUNCTYPE(ctypes.c_int32, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_uint64, ctypes.c_void_p)
 
@@ -97,6 +97,8 @@ def lib():
         L.sg2v_plan_describe_n.argtypes = [i64, i64, vp, ctypes.c_int, vp, u64, P(u64)]
         L.sg2v_estimate.argtypes = [vp, i64, vp, P(ctypes.c_double)]
         L.sg2v_profile_read_launches.argtypes = [i64, vp, vp, vp, vp, vp, P(i64)]
+        L.sg2v_partition_relabel.argtypes = [i64, vp, vp, i32, vp, vp, vp]
+        L.sg2v_graph_set_vertex_ids.argtypes = [vp, vp, i64]
         L.sg2v_profile_enable.argtypes = [i32]
         L.sg2v_profile_read.argtypes = [vp, vp, vp]
         L.sg2v_last_error.restype = ctypes.c_char_p
@@ -106,7 +108,8 @@ def lib():
                      "sg2v_plan_describe", "sg2v_plan_describe_n", "sg2v_profile_enable", "sg2v_profile_read",
                      "sg2v_count_batch", "sg2v_workspace_bytes_batch", "sg2v_comm_unique_id",
                      "sg2v_comm_init_nccl", "sg2v_comm_init_callback", "sg2v_graph_load_partition",
-                     "sg2v_estimate", "sg2v_profile_read_launches"):
+                     "sg2v_estimate", "sg2v_profile_read_launches", "sg2v_partition_relabel",
+                     "sg2v_graph_set_vertex_ids"):
             getattr(L, name).restype = ctypes.c_int
         _lib = L
     return _lib
@@ -440,6 +443,24 @@ def partition_rows(n_global: int, rank: int, world: int):
     nl = (n_global + world - 1) // world
     begin = min(rank * nl, n_global)
     return begin, max(0, min(nl, n_global - begin))
+
+
+def partition_relabel(row_offsets, col_indices, world):
+    """sg2v_partition_relabel: (old_of_new, relabelled row_offsets, col_indices)."""
+    ro = np.ascontiguousarray(row_offsets, dtype=np.int64)
+    ci = np.ascontiguousarray(col_indices, dtype=np.int32)
+    n = ro.size - 1
+    oon = np.empty(max(n, 1), np.int32)
+    ro2 = np.empty(n + 1, np.int64)
+    ci2 = np.empty(max(ci.size, 1), np.int32)
+    _check(lib().sg2v_partition_relabel(n, ro.ctypes.data, ci.ctypes.data if ci.size else None, int(world),
+                                        oon.ctypes.data, ro2.ctypes.data, ci2.ctypes.data))
+    return oon[:n], ro2, ci2[:ci.size]
+
+
+def graph_set_vertex_ids(graph: Graph, orig_ids) -> None:
+    ids = np.ascontiguousarray(orig_ids, dtype=np.int32)
+    _check(lib().sg2v_graph_set_vertex_ids(graph.handle, ids.ctypes.data if ids.size else None, int(ids.size)))
 
 
 def graph_load_partition(n_global, row_begin, n_local, row_offsets, col_indices, stream=None) -> Graph:

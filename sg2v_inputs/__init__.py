@@ -14,6 +14,7 @@ from .graphs import (  # noqa: F401
     rmat_1m_like,
     miami_like,
     orkut_like,
+    graph500_like,
     BIG_GRAPHS,
     cycle_graph,
     path_graph,

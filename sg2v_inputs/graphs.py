@@ -211,4 +211,14 @@ def orkut_like(seed: int = 1) -> CSR:
     return g
 
 
-BIG_GRAPHS = {"rmat1m": lambda: rmat_1m_like(), "miami": lambda: miami_like(), "orkut": lambda: orkut_like()}
+def graph500_like(scale: int = 22, edge_factor: int = 16, seed: int = 1) -> CSR:
+    """SURVEY §8(d) D5a (strong-scaling graph): Graph500 RMAT(0.57, 0.19, 0.19, 0.05),
+    scale 22, edge factor 16 (m = 16·2^scale drawn edges), id-permuted — shaped like the
+    paper's GS22 row (2M vertices / 128M edges / avg 53 / max 170K)."""
+    g = rmat(scale, edge_factor << scale, 0.57, 0.19, 0.19, seed=seed, perm_seed=7)
+    g.name = f"Graph500-like(scale={scale},ef={edge_factor},seed={seed})"
+    return g
+
+
+BIG_GRAPHS = {"rmat1m": lambda: rmat_1m_like(), "miami": lambda: miami_like(), "orkut": lambda: orkut_like(),
+              "gs22": lambda: graph500_like()}

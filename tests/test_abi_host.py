@@ -201,3 +201,36 @@ def test_library_alpha_matches_enumeration():
             assert name.startswith("star")
             a = math.factorial(k - 1)
         assert sg.template_build(k, e).info()["alpha"] == a, name
+
+
+def test_partition_relabel_is_a_balanced_isomorphism(oracle):
+    """sg2v_partition_relabel (vertex mode): the relabelled CSR is the same
+    graph (colouring by input id gives the oracle's counts), blocks keep the rank-row
+    contract, and their edge counts are balanced far better than the uniform split."""
+    import numpy as np
+    from sg2v_inputs import rmat, TEMPLATES
+    g = rmat(13, 120_000, 0.57, 0.19, 0.19, seed=9)   # Graph500-skewed, unpermuted hubs
+    for world in (2, 3, 8):
+        oon, ro2, ci2 = sg.partition_relabel(g.row_offsets, g.col_indices, world)
+        assert sorted(oon.tolist()) == list(range(g.n))
+        # same edge set under the map
+        new_of_old = np.empty(g.n, np.int64)
+        new_of_old[oon] = np.arange(g.n)
+        e1 = {(int(new_of_old[a]), int(new_of_old[b])) for a, b in g.edges()}
+        rows = np.repeat(np.arange(g.n), np.diff(ro2))
+        e2 = {(int(a), int(b)) for a, b in zip(rows, ci2) if a < b}
+        e1 = {(min(a, b), max(a, b)) for a, b in e1}
+        assert e1 == e2
+        assert all(np.all(np.diff(ci2[ro2[u]:ro2[u + 1]]) > 0) for u in range(0, g.n, 97))
+        nl = -(-g.n // world)
+        blk = [int(ro2[min(g.n, (r + 1) * nl)] - ro2[min(g.n, r * nl)]) for r in range(world)]
+        uni = [int(g.row_offsets[min(g.n, (r + 1) * nl)] - g.row_offsets[min(g.n, r * nl)]) for r in range(world)]
+        assert max(blk) / (g.nnz / world) <= 1.02, blk
+        assert max(blk) - min(blk) <= max(uni) - min(uni)
+    # colouring by input id: the relabelled graph's counts are the input graph's
+    from sg2v_inputs import CSR
+    oon, ro2, ci2 = sg.partition_relabel(g.row_offsets, g.col_indices, 4)
+    gr = CSR(n=g.n, row_offsets=ro2, col_indices=ci2)
+    e = TEMPLATES["u5-2"]
+    cols = oracle.colors(3, 1, g.n, 5)
+    assert oracle.count(gr, 5, e, cols[oon]) == oracle.count(g, 5, e, cols)

@@ -90,12 +90,22 @@ def _worker(rank, world, port, q):
     g = rmat(12, 60_000, 0.45, 0.22, 0.22, seed=6)
     b, nl, ro, ci = _part(g, rank, world)
     Gp = sgw.graph_load_partition(g.n, b, nl, ro, ci)
+    # the balanced relabelling (degree-dealt blocks), colours keyed by the input ids
+    oon, ro2, ci2 = sgw.partition_relabel(g.row_offsets, g.col_indices, world)
+    Gr = sgw.graph_load_partition(g.n, b, nl, ro2[b:b + nl + 1] - ro2[b], ci2[ro2[b]:ro2[b + nl]])
+    sgw.graph_set_vertex_ids(Gr, oon)
     res = {}
     for name in ("u5-2", "u7-2", "u10-2"):
         e = TEMPLATES[name]
         T = sgw.template_build(_k(e), e)
+        # column tiles (overlapped exchange) and whole rows (fused kernels on staged rows)
         _, c = sgw.count(Gp, T, n_iter=2, seed=5, precision="u64", comm=comm, col_tile=16)
+        _, c0 = sgw.count(Gp, T, n_iter=2, seed=5, precision="u64", comm=comm, col_tile=0)
+        _, cr = sgw.count(Gr, T, n_iter=2, seed=5, precision="u64", comm=comm, col_tile=0)
+        _, cf = sgw.count(Gr, T, n_iter=2, seed=5, precision="f32", comm=comm, col_tile=0)
+        assert [int(x) for x in c] == [int(x) for x in c0] == [int(x) for x in cr], name
         res[name] = [int(x) for x in c]
+        res[name + "/f32"] = [float(x) for x in cf]
     comm.free()
     dist.barrier()
     dist.destroy_process_group()
@@ -122,3 +132,6 @@ def test_world2_callback_equals_single(oracle):
         assert out[0][name] == [int(x) for x in want] == out[1][name], name
         k = _k(e)
         assert out[0][name] == [oracle.count(g, k, e, oracle.colors(5, j, g.n, k)) for j in range(2)], name
+        for j in range(2):
+            wf = oracle.count(g, k, e, oracle.colors(5, j, g.n, k), arith=oracle.ARITH_F64)[0]
+            assert abs(out[0][name + "/f32"][j] - wf) <= 1e-4 * wf, name
