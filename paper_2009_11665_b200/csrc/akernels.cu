@@ -659,11 +659,15 @@ static int launch_astep_heavy(const AStepArgs &A, int64_t nvec, void *stream) {
 // register budget, and a consumer spends ~6 instructions per 16-B vector instead of
 // the register-gather's index/policy/address work per neighbour.
 // ---------------------------------------------------------------------------
-static constexpr int kBulkConsumers = 256;
-static constexpr int kBulkThreads = kBulkConsumers + 32;
+// NC consumer threads (64, 128 or 256: sized to the row) + one producer warp.
+template <int NC>
+struct BulkMinBlocks {
+    static constexpr int value = NC == 256 ? 3 : NC == 128 ? 5 : 8;
+};
 
-template <typename T, typename RT, int R>
-__global__ void __launch_bounds__(kBulkThreads, 3) astep_bulk_kernel(AStepArgs A, int S, uint32_t stage_bytes) {
+template <typename T, typename RT, int R, int NC>
+__global__ void __launch_bounds__(NC + 32, BulkMinBlocks<NC>::value) astep_bulk_kernel(AStepArgs A, int S, uint32_t stage_bytes) {
+    constexpr int kBulkConsumers = NC;
     constexpr int VN = Vec<T>::N;
     constexpr int32_t kIdMask = (1 << kClassShift) - 1;
     extern __shared__ __align__(128) unsigned char smem[];
@@ -871,14 +875,16 @@ static int launch_astep_t(const AStepArgs &A, void *stream) {
 
 // Bulk-staged launch (astep_bulk_kernel): R 16-B vectors per consumer lane, S stages
 // sized for ~48 KB of bulk copies in flight per CTA (3 CTAs per SM).
-template <typename T, typename RT, int R>
+template <typename T, typename RT, int R, int NC>
 static int launch_astep_bulk_t(const AStepArgs &A, void *stream) {
+    constexpr int kBulkThreads = NC + 32;
     constexpr int VN = Vec<T>::N;
     const int64_t nvec_p = (A.ldseg_p > 0 ? A.ldseg_p : A.ldp) / VN;
     const uint32_t stage_bytes = (uint32_t)(((nvec_p * 16) + 127) / 128 * 128);
-    static int want_kb = -1;  // SG2V_BULK_KB (experiments): bulk bytes in flight per CTA
+    static int want_kb = -1;  // SG2V_BULK_KB (experiments): bulk bytes in flight per 256 consumers
     if (want_kb < 0) { const char *e = getenv("SG2V_BULK_KB"); want_kb = e ? atoi(e) : 48; }
-    int S = (int)std::max<int64_t>(3, std::min<int64_t>(16, ((int64_t)want_kb * 1024) / stage_bytes));
+    const int64_t kb = std::max<int64_t>(8, (int64_t)want_kb * NC / 256);
+    int S = (int)std::max<int64_t>(3, std::min<int64_t>(16, (kb * 1024) / stage_bytes));
     auto smem_of = [&](int s) {
         return (size_t)((2 * s * 8 + 127) / 128 * 128) + (size_t)((A.smem_group * sizeof(T) + 127) / 128 * 128) +
                (size_t)s * stage_bytes;
@@ -886,7 +892,7 @@ static int launch_astep_bulk_t(const AStepArgs &A, void *stream) {
     while (S > 3 && smem_of(S) > 220 * 1024) --S;
     const size_t smem = smem_of(S);
     if (smem > 227 * 1024) return -1;
-    auto kern = astep_bulk_kernel<T, RT, R>;
+    auto kern = astep_bulk_kernel<T, RT, R, NC>;
     if (cudaError_t e = ensure_dyn_smem((const void *)kern, smem)) return (int)e;
     int occ = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kBulkThreads, smem);
@@ -953,19 +959,21 @@ static int launch_astep_cfg(const AStepArgs &A0, void *stream) {
         const char *e = getenv("SG2V_BULK");
         bulk = e ? atoi(e) : 1;
         const char *m = getenv("SG2V_BULK_MIN");
-        bulk_min = m ? atoi(m) : 128;
+        bulk_min = m ? atoi(m) : 64;
     }
     if (MODE == 0 && bulk && !multi && !A.src_hist && A.pmap != nullptr && nvec >= bulk_min && nvec <= 2048) {
-        if (nvec <= 256) return launch_astep_bulk_t<T, RT, 1>(A, stream);
-        if (nvec <= 512) return launch_astep_bulk_t<T, RT, 2>(A, stream);
-        if (nvec <= 1024) return launch_astep_bulk_t<T, RT, 4>(A, stream);
-        return launch_astep_bulk_t<T, RT, 8>(A, stream);
+        if (nvec <= 64) return launch_astep_bulk_t<T, RT, 1, 64>(A, stream);
+        if (nvec <= 128) return launch_astep_bulk_t<T, RT, 1, 128>(A, stream);
+        if (nvec <= 256) return launch_astep_bulk_t<T, RT, 1, 256>(A, stream);
+        if (nvec <= 512) return launch_astep_bulk_t<T, RT, 2, 256>(A, stream);
+        if (nvec <= 1024) return launch_astep_bulk_t<T, RT, 4, 256>(A, stream);
+        return launch_astep_bulk_t<T, RT, 8, 256>(A, stream);
     }
     // heavy rows of narrow register-gather steps: CTA per row first, the rest after
     // (SG2V_HEAVY=0 disables)
     static int heavy = -1;
     if (heavy < 0) { const char *e = getenv("SG2V_HEAVY"); heavy = e ? atoi(e) : 1; }
-    if (MODE == 0 && heavy && !multi && !A.src_hist && A.pmap != nullptr && gt < 256 && nvec <= 128 &&
+    if (MODE == 0 && heavy && !multi && !A.src_hist && A.pmap != nullptr && gt < 256 && nvec <= 32 &&
         A.n_heavy > 0 && A.n_heavy < A.n) {
         AStepArgs H = A;
         H.n = A.n_heavy;

@@ -12,6 +12,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <functional>
 #include <limits>
@@ -587,6 +588,51 @@ static bool plan_chain(const Template &t, const Chain &c, int root, int64_t n, i
     return true;
 }
 
+// Shared-memory bank schedule of the split terms of a GENERAL step (eMA).
+// In the V-row eMA each lane owns one output o and reads, per term, the 16-B entries
+// M_a(·, ia) and B(·, ib) of its V interleaved rows; a 128-bit shared load is served a
+// quarter-warp (8 lanes = 8 consecutive outputs) at a time and is conflict-free only if
+// the 8 entries fall in distinct 16-B bank groups (entry mod 8).  The sum over a
+// row's terms is order-free (exact in U64; a fixed order in F32/F64), so the terms of
+// each output are permuted, quarter by quarter and step by step, to spread both
+// operands over the 8 groups (greedy over 8 x 8 (group_a, group_b) buckets).
+// SG2V_EMA_SCHED=0 keeps the natural subset order (experiments).
+static void schedule_terms(std::vector<std::pair<int32_t, int32_t>> &pairs, int64_t cs, int64_t nt, int64_t aoff) {
+    static int on = -1;
+    if (on < 0) { const char *e = getenv("SG2V_EMA_SCHED"); on = e ? atoi(e) : 1; }
+    if (!on) return;
+    std::vector<std::pair<int32_t, int32_t>> out(pairs.size());
+    for (int64_t o0 = 0; o0 < cs; o0 += 8) {
+        const int L = (int)std::min<int64_t>(8, cs - o0);
+        // per lane: terms bucketed by (group of M_a entry, group of B entry)
+        std::vector<std::vector<int64_t>> bucket((size_t)L * 64);
+        for (int l = 0; l < L; ++l)
+            for (int64_t w = 0; w < nt; ++w) {
+                const auto &pq = pairs[(size_t)((o0 + l) * nt + w)];
+                const int ga = (int)((aoff + pq.first) & 7), gb = (int)(pq.second & 7);
+                bucket[(size_t)l * 64 + ga * 8 + gb].push_back(w);
+            }
+        for (int64_t w = 0; w < nt; ++w) {
+            unsigned usedA = 0, usedB = 0;
+            for (int l = 0; l < L; ++l) {
+                int best = -1, bestc = 99;
+                for (int b = 0; b < 64 && bestc > 0; ++b) {
+                    if (bucket[(size_t)l * 64 + b].empty()) continue;
+                    const int c = ((usedA >> (b >> 3)) & 1) + ((usedB >> (b & 7)) & 1);
+                    if (c < bestc) { bestc = c; best = b; }
+                }
+                auto &bk = bucket[(size_t)l * 64 + best];
+                const int64_t src = bk.back();
+                bk.pop_back();
+                out[(size_t)((o0 + l) * nt + w)] = pairs[(size_t)((o0 + l) * nt + src)];
+                usedA |= 1u << (best >> 3);
+                usedB |= 1u << (best & 7);
+            }
+        }
+    }
+    pairs.swap(out);
+}
+
 static bool build_index(Plan &pl) {
     const int k = pl.k;
     const uint32_t full = (k == 32) ? 0xffffffffu : ((1u << k) - 1);
@@ -719,6 +765,7 @@ static bool build_index(Plan &pl) {
             } else {
                 st.packed = (st.ca < 65536 && st.cb < 65536) ? 1 : 0;
                 const int64_t cs = st.cs, nt = st.nterms;
+                if (!st.top && nt >= 8) schedule_terms(pairs, cs, nt, st.self_a ? 0 : st.ldb);
                 if (st.packed) {
                     size_t base = pl.index.size();
                     pl.index.resize(base + (size_t)(cs * nt));
