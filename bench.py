@@ -230,7 +230,7 @@ def run_reference(args):
 
 # --------------------------------------------------------------------------- roofline
 SMEM_B_PER_CLK_SM = 128      # shared-memory bandwidth per SM (B200_PROFILING.md / B300_MICROARCH.md)
-EMA_BYTES_PER_TERM = 8       # each split term reads M_a(i,I_a) and B(i,I_p) from shared memory (fp32)
+# each split term reads M_a(i,I_a) and B(i,I_p) from shared memory: 2 x element bytes
 FMA_PER_CLK_SM = 128         # fp32 FMA lanes per SM
 
 
@@ -317,7 +317,7 @@ def roofline(args, prof, recs, plan):
     if gen:
         t_ms = sum(r["ms"] for r in gen)
         terms = sum(r["ema_terms"] for r in gen)
-        smem_roof = 148 * SMEM_B_PER_CLK_SM * sm_mhz * 1e6 / EMA_BYTES_PER_TERM
+        smem_roof = 148 * SMEM_B_PER_CLK_SM * sm_mhz * 1e6 / (2 * plan["elem"])
         fma_roof = 148 * FMA_PER_CLK_SM * sm_mhz * 1e6
         rate = terms / (t_ms / 1e3) if t_ms > 0 else 0.0
         ema = {"terms_per_colouring": terms / max(len(cols), 1), "ms_per_colouring": t_ms / max(len(cols), 1),
@@ -399,16 +399,13 @@ def run_sg2v(args):
     overflow = []  # colourings whose F32 count overflowed (EOVERFLOW), reported in the line
 
     def count(GG, n_iter, off, stride=1, wsp=None):
+        # one DP run per colouring: EOVERFLOW (an F32 table entry overflowed) is recorded, not retried
         wsp = ws if wsp is None else wsp
-        try:
-            return sg.count(GG, T, n_iter=n_iter, seed=args.seed, iter_offset=off, iter_stride=stride,
-                            precision=args.precision, workspace=wsp, layout=args.layout)
-        except sg.Sg2vError as ex:
-            if ex.code != sg.sg2v.EOVERFLOW:
-                raise
+        r = sg.count(GG, T, n_iter=n_iter, seed=args.seed, iter_offset=off, iter_stride=stride,
+                     precision=args.precision, workspace=wsp, layout=args.layout, allow_overflow=True)
+        if sg.sg2v.LAST_STATUS == sg.sg2v.EOVERFLOW:
             overflow.append(off)
-            return sg.count(GG, T, n_iter=n_iter, seed=args.seed, iter_offset=off, iter_stride=stride,
-                            precision=args.precision, workspace=wsp, layout=args.layout, allow_overflow=True)
+        return r
 
     # warm-up (untimed)
     for t in range(args.warmup):
@@ -489,7 +486,7 @@ def run_sg2v(args):
                    "l2": "inputs larger than L2 (CSR %.2f GB + count tables %.1f GB >> 126 MB); no flush"
                          % (g.nbytes() / 1e9, plan["tables_bytes"] / 1e9)},
         "estimate": est, "colorful_first": float(c[0]),
-        "status": "EOVERFLOW" if overflow else "OK", "overflowed_colourings": len(overflow),
+        "status": "EOVERFLOW" if overflow else "OK", "overflowed_calls": len(overflow),
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(g.nbytes()),
                 "d2h_bytes_per_step": 8},
         "gpu_launches": int(launches),
@@ -501,7 +498,7 @@ def run_sg2v(args):
     if ema:
         line["ema"] = ema
     if world == 1 and not args.no_cpu_baseline:
-        per, desc, cores = cpu_sample(args, k, edges, g.n, g.nnz, steps=1)
+        per, desc, cores = cpu_sample(args, k, edges, g.n, g.nnz, steps=1, target_s=20.0)
         line["cpu_baseline"] = {"value": per[0], "unit": UNIT, "cores": cores, "kind": "oracle", "sample": desc}
         full = full_graph_oracle_record(args.template, args.scale)
         if full:

@@ -127,7 +127,7 @@ struct AStepArgs {
     int64_t aoff;       // offset of the M_a row in a group's shared memory: ldb, or 0 when
                         // M_a(i,·) IS B(i,·) (self step: T_s = root + two copies of X)
     // vertex-partitioned mode: B rows live in global memory
-    int64_t cp_map;     // row length of the push map (= cp unless tiled)
+    int64_t cp_map;     // row stride of the push map: cp rounded up to 4 entries
     int64_t u0;         // first passive column of this tile (push-map offset)
     int tile_mode;      // stage 1 only: gather a staged column tile, push into bg rows
     int bsrc_global;    // stage 1 = copy the completed B row from bg
@@ -152,6 +152,19 @@ __device__ __forceinline__ bool nonfinite4(const uint4 &w) {
         return !isfinite(__uint_as_float(w.x)) || !isfinite(__uint_as_float(w.y)) ||
                !isfinite(__uint_as_float(w.z)) || !isfinite(__uint_as_float(w.w));
     else return false;
+}
+
+// push targets of the VN elements of 16-B vector v (one aligned vector load of the
+// padded push-map row; -1 = the set contains c(i), nothing to add)
+template <typename T>
+__device__ __forceinline__ void load_targets(const int32_t *mp, int64_t v, int32_t (&tt)[Vec<T>::N]) {
+    if constexpr (Vec<T>::N == 4) {
+        const int4 q = __ldg(reinterpret_cast<const int4 *>(mp) + v);
+        tt[0] = q.x; tt[1] = q.y; tt[2] = q.z; tt[3] = q.w;
+    } else {
+        const int2 q = __ldg(reinterpret_cast<const int2 *>(mp) + v);
+        tt[0] = q.x; tt[1] = q.y;
+    }
 }
 
 // ---- stage 1 for one row: B(i,·) over T ⊂ [k]∖{c(i)} into sB (group-uniform) ----
@@ -181,10 +194,12 @@ __device__ __forceinline__ void gather_row(const AStepArgs &A, int64_t i, int ci
             for (int64_t v0 = 0; v0 < nvec_p; v0 += GT * R) {
                 uint4 acc[R];
                 bool need[R];
+                int32_t tt[R][VN];  // push targets, loaded before the neighbour loads
 #pragma unroll
                 for (int q = 0; q < R; ++q) {
                     acc[q] = make_uint4(0, 0, 0, 0);
                     need[q] = v0 + q * GT + t < nvec_p;
+                    if (need[q]) load_targets<T>(mp, v0 + q * GT + t, tt[q]);
                 }
                 int64_t e2 = e;
                 const int64_t e3 = e + cnt;
@@ -240,16 +255,10 @@ __device__ __forceinline__ void gather_row(const AStepArgs &A, int64_t i, int ci
                 // push R_x into B: distinct targets within one colour
 #pragma unroll
                 for (int q = 0; q < R; ++q) {
-                    const int64_t v = v0 + q * GT + t;
                     if (need[q]) {
 #pragma unroll
-                        for (int el = 0; el < VN; ++el) {
-                            const int64_t u = v * VN + el;
-                            if (u < A.cp) {
-                                const int32_t tt = __ldg(mp + u);
-                                if (tt >= 0) sB[(size_t)tt * STRIDE] += vget<T>(acc[q], el);
-                            }
-                        }
+                        for (int el = 0; el < VN; ++el)
+                            if (tt[q][el] >= 0) sB[(size_t)tt[q][el] * STRIDE] += vget<T>(acc[q], el);
                     }
                 }
             }
@@ -598,16 +607,13 @@ __global__ void __launch_bounds__(256) astep_heavy_kernel(AStepArgs A) {
                 const int32_t *mp = A.pmap + ((size_t)x * k + ci) * A.cp_map + A.u0;
                 for (int64_t v = t; v < nvec_p; v += 256) {
                     const int q = (int)(v / SG), ll = (int)(v % SG);
+                    int32_t tt[VN];
+                    load_targets<T>(mp, v, tt);
                     uint4 sum = scratch[q * SG + ll];
                     for (int g2 = 1; g2 < NG; ++g2) Vec<T>::add(sum, scratch[(size_t)g2 * SG * R + q * SG + ll]);
 #pragma unroll
-                    for (int el = 0; el < VN; ++el) {
-                        const int64_t u = v * VN + el;
-                        if (u < A.cp) {
-                            const int32_t tt = __ldg(mp + u);
-                            if (tt >= 0) sB[tt] += vget<T>(sum, el);
-                        }
-                    }
+                    for (int el = 0; el < VN; ++el)
+                        if (tt[el] >= 0) sB[tt[el]] += vget<T>(sum, el);
                 }
                 group_sync<256>(0);
             }
@@ -760,8 +766,15 @@ __global__ void __launch_bounds__(NC + 32, BulkMinBlocks<NC>::value) astep_bulk_
             const int cnt = __ldg(h + x);
             if (x == ci || cnt == 0) continue;
             uint4 acc[R];
+            // push targets of this colour, loaded before the stages are consumed
+            const int32_t *mp = A.pmap + ((size_t)x * k + ci) * A.cp_map + A.u0;
+            int32_t tt[R][VN];
 #pragma unroll
-            for (int q = 0; q < R; ++q) acc[q] = make_uint4(0, 0, 0, 0);
+            for (int q = 0; q < R; ++q) {
+                acc[q] = make_uint4(0, 0, 0, 0);
+                const int v = t + q * kBulkConsumers;
+                if (v < nvec_p) load_targets<T>(mp, v, tt[q]);
+            }
             for (int c = 0; c < cnt; ++c) {
                 mbar_wait(full + slot, ph);
                 const unsigned char *st = stages + (size_t)slot * stage_bytes;
@@ -775,19 +788,13 @@ __global__ void __launch_bounds__(NC + 32, BulkMinBlocks<NC>::value) astep_bulk_
                 if (++slot == S) { slot = 0; ph ^= 1; }
             }
             // push R_x into B: distinct targets within one colour
-            const int32_t *mp = A.pmap + ((size_t)x * k + ci) * A.cp_map + A.u0;
 #pragma unroll
             for (int q = 0; q < R; ++q) {
                 const int64_t v = t + q * kBulkConsumers;
                 if (v < nvec_p) {
 #pragma unroll
-                    for (int el = 0; el < VN; ++el) {
-                        const int64_t u = v * VN + el;
-                        if (u < A.cp) {
-                            const int32_t tt = __ldg(mp + u);
-                            if (tt >= 0) sB[tt] += vget<T>(acc[q], el);
-                        }
-                    }
+                    for (int el = 0; el < VN; ++el)
+                        if (tt[q][el] >= 0) sB[tt[q][el]] += vget<T>(acc[q], el);
                 }
             }
             group_sync<kBulkConsumers>(0);  // colours x and x' may push to the same T
@@ -1086,7 +1093,7 @@ int launch_astep_vp(const Graph &g, const Plan &pl, const Step &st, const uint8_
     A.nterms = st.nterms;
     A.rowval = rowval;
     A.packed = st.packed;
-    A.cp_map = st.cp;
+    A.cp_map = (st.cp + 3) / 4 * 4;  // push-map rows are padded to 4 entries
     A.u0 = 0;
     A.tile_mode = 0;
     A.bsrc_global = 0;

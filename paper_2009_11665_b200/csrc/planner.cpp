@@ -598,8 +598,9 @@ static bool plan_chain(const Template &t, const Chain &c, int root, int64_t n, i
 // operands over the 8 groups (greedy over 8 x 8 (group_a, group_b) buckets).
 // SG2V_EMA_SCHED=0 keeps the natural subset order (experiments).
 static void schedule_terms(std::vector<std::pair<int32_t, int32_t>> &pairs, int64_t cs, int64_t nt, int64_t aoff) {
-    static int on = -1;
-    if (on < 0) { const char *e = getenv("SG2V_EMA_SCHED"); on = e ? atoi(e) : 1; }
+    static int on = -1;  // off by default: measured slower (u17 10 = 5 + 5: 780 -> 911 ms), the natural
+                         // subset order lets adjacent outputs share entries (broadcast reads)
+    if (on < 0) { const char *e = getenv("SG2V_EMA_SCHED"); on = e ? atoi(e) : 0; }
     if (!on) return;
     std::vector<std::pair<int32_t, int32_t>> out(pairs.size());
     for (int64_t o0 = 0; o0 < cs; o0 += 8) {
@@ -643,6 +644,11 @@ static bool build_index(Plan &pl) {
     auto align = [&]() { while (pl.index.size() % 4) pl.index.push_back(0); };
     std::map<int, int64_t> push_maps;               // anchored push map per passive size p
     std::map<int, int64_t> push_maps_x;             // ... for exclusion-projected sources
+    // push-map rows [x][ci] are padded to a multiple of 4 entries (-1), so a lane reads the
+    // targets of its 16-B vector with one aligned 16-B (F32) / 8-B (F64, U64) load
+    auto pad_row = [&](size_t len) {
+        for (size_t q = len; q % 4; ++q) pl.index.push_back(-1);
+    };
     for (Step &st : pl.steps) {
         // ---- projected output: write map ----
         if (st.proj_out) {
@@ -675,7 +681,7 @@ static bool build_index(Plan &pl) {
                 std::vector<uint32_t> us;  // (p-1)-subsets of [k] \ {x, ci}, relabelled into [k-2]
                 for_each_subset(k - 2, st.p - 1, [&](uint32_t m) { us.push_back(m); });
                 for (int x = 0; x < k; ++x)
-                    for (int ci = 0; ci < k; ++ci)
+                    for (int ci = 0; ci < k; ++ci) {
                         for (uint32_t u : us) {
                             int32_t tcol = -1;
                             if (x != ci) {
@@ -685,6 +691,8 @@ static bool build_index(Plan &pl) {
                             }
                             pl.index.push_back(tcol);
                         }
+                        pad_row(us.size());
+                    }
                 push_maps_x[st.p] = st.map_off;
             }
         } else if (anch && st.src == SRC_GATHER && ((pl.vp && !pl.vp_full) || !(st.top && st.comb == COMB_ACTIVE_LEAF))) {
@@ -699,7 +707,7 @@ static bool build_index(Plan &pl) {
                 std::vector<uint32_t> us;
                 for_each_subset(k - 1, st.p - 1, [&](uint32_t m) { us.push_back(m); });
                 for (int x = 0; x < k; ++x)
-                    for (int ci = 0; ci < k; ++ci)
+                    for (int ci = 0; ci < k; ++ci) {
                         for (uint32_t u : us) {
                             int32_t tcol = -1;
                             if (x != ci) {
@@ -709,6 +717,8 @@ static bool build_index(Plan &pl) {
                             }
                             pl.index.push_back(tcol);
                         }
+                        pad_row(us.size());
+                    }
                 push_maps[st.p] = st.map_off;
             }
         }

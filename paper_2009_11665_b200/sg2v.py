@@ -318,10 +318,15 @@ def count(graph: Graph, tmpl: Template, n_iter: int, seed: int, precision="f32",
         out = np.zeros(n_iter, dtype=np.float64)
         rc = lib().sg2v_count_ex(graph.handle, tmpl.handle, tmpl.k, int(n_iter), int(seed) & (2**64 - 1),
                                  ctypes.byref(o), ctypes.byref(est), out.ctypes.data, None)
+    global LAST_STATUS
+    LAST_STATUS = rc
     if rc == EOVERFLOW and allow_overflow:
         return est.value, out
     _check(rc)
     return est.value, out
+
+
+LAST_STATUS = OK  # status of the last count() / count_batch() (EOVERFLOW with allow_overflow=True)
 
 
 def estimate(tmpl: Template, colorful) -> float:

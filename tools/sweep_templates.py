@@ -34,7 +34,13 @@ for name in names:
             s1.record()
             torch.cuda.synchronize()
             p = sg.profile_read()
+            recs = sg.profile_read_launches()
             sg.profile_enable(False)
+            gen = [r for r in recs if r["ema_terms"] > 0]
+            gms = sum(r["ms"] for r in gen)
+            terms = sum(r["ema_terms"] for r in gen)
+            # shared-memory roof of the eMA: 148 SMs x 128 B/clk / 8 B per term (two fp32 operands)
+            ema_roof = 148 * 128 * 1965e6 / 8
             dt = s0.elapsed_time(s1) / 3e3
             b = p["step"]["bytes"] + p["top"]["bytes"]
             ms = p["step"]["ms"] + p["top"]["ms"]
@@ -42,6 +48,10 @@ for name in names:
             print(json.dumps({"template": name, "k": k, "precision": prec, "s_per_colouring": dt,
                               "steps": len(d["steps"]), "root": d["root"], "workspace_GB": d["workspace_bytes"] / 1e9,
                               "alg_GBps": b / ms / 1e6 if ms else 0, "frac": b / ms / 1e6 / peak if ms else 0,
+                              "impl_frac": sum(r["impl_bytes"] for r in recs if r["cls"] in ("step", "top")) / ms / 1e6 / peak if ms else 0,
+                              "ema_terms_per_s": terms / gms * 1e3 if gms else None,
+                              "ema_frac_smem": terms / gms * 1e3 / ema_roof if gms else None,
+                              "ema_ms": gms / 3,
                               "finite": finite, "colorful0": float(c[0])}), flush=True)
             del ws
             torch.cuda.empty_cache()
