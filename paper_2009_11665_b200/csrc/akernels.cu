@@ -134,6 +134,11 @@ struct AStepArgs {
     char *bg;           // [n_local][ldb] B rows (tile_mode / bsrc_global)
     int *ovf;           // F32 overflow flag of this sg2v_count call (in its workspace)
     int64_t n_heavy;    // rows [0, n_heavy) of `order` have >= 2^kHeavyLog2 neighbours
+    // split eMA pipeline (GENERAL eMA-heavy steps): the gather launch stores each finished
+    // B row at b_out + r·ldb (r = position in `order`) instead of running the eMA; the
+    // combine launch (MODE 2) reads bg by that position (bg_pos)
+    char *b_out;
+    int bg_pos;
 };
 
 // F32 overflow flag (AStepArgs::ovf, one int in the calling sg2v_count's workspace, so
@@ -481,7 +486,8 @@ __global__ void __launch_bounds__(256, AStepMinBlocks<U, V, MODE>::value) astep_
             }
             if (actv[0]) {
                 if (MODE == 2) {
-                    const char *b = A.bg + (size_t)i * A.ldb * sizeof(T);
+                    const int64_t br = A.bg_pos ? (slot * G + g) : i;
+                    const char *b = A.bg + (size_t)br * A.ldb * sizeof(T);
                     for (int64_t q = t; q < A.ldb / VN; q += GT) reinterpret_cast<uint4 *>(sB)[q] = ldg16(b + q * 16);
                 } else {
                     for (int64_t q = t; q < A.ldb / VN; q += GT) reinterpret_cast<uint4 *>(sB)[q] = make_uint4(0, 0, 0, 0);
@@ -493,6 +499,15 @@ __global__ void __launch_bounds__(256, AStepMinBlocks<U, V, MODE>::value) astep_
             }
             group_sync<GT>(g);
             if (MODE == 0 && actv[0]) gather_row<T, GT, R, U>(A, i, (int)A.colors[i], sB, t, g, pol_last, pol_first);
+            if (MODE == 0 && A.b_out) {  // split pipeline: hand the B row to the eMA launch
+                group_sync<GT>(g);
+                if (actv[0]) {
+                    uint4 *o = reinterpret_cast<uint4 *>(A.b_out + (size_t)(slot * G + g) * A.ldb * sizeof(T));
+                    for (int64_t q = t; q < A.ldb / VN; q += GT) __stcg(o + q, reinterpret_cast<const uint4 *>(sB)[q]);
+                }
+                group_sync<GT>(g);
+                continue;
+            }
         } else {
             static_assert(MODE != 1, "tile mode runs one row per group");
 #pragma unroll
@@ -500,7 +515,8 @@ __global__ void __launch_bounds__(256, AStepMinBlocks<U, V, MODE>::value) astep_
                 const int64_t i = iv[v];
                 if (actv[v]) {
                     if (MODE == 2) {
-                        const T *b = reinterpret_cast<const T *>(A.bg) + (size_t)i * A.ldb;
+                        const int64_t br = A.bg_pos ? (slot * G + g) * V + v : i;
+                        const T *b = reinterpret_cast<const T *>(A.bg) + (size_t)br * A.ldb;
                         for (int64_t q = t; q < A.ldb; q += GT) sBase[q * V + v] = b[q];
                     } else {
                         for (int64_t q = t; q < A.ldb; q += GT) sBase[q * V + v] = 0;
@@ -799,7 +815,12 @@ __global__ void __launch_bounds__(NC + 32, BulkMinBlocks<NC>::value) astep_bulk_
             }
             group_sync<kBulkConsumers>(0);  // colours x and x' may push to the same T
         }
-        ema_stage<T, RT, kBulkConsumers, 1>(A, sB, iv, actv, t, 0, red, bad);
+        if (A.b_out) {  // split pipeline: hand the B row to the eMA launch
+            uint4 *o = reinterpret_cast<uint4 *>(A.b_out + (size_t)r * A.ldb * sizeof(T));
+            for (int64_t q = t; q < A.ldb / VN; q += kBulkConsumers) __stcg(o + q, reinterpret_cast<const uint4 *>(sB)[q]);
+        } else {
+            ema_stage<T, RT, kBulkConsumers, 1>(A, sB, iv, actv, t, 0, red, bad);
+        }
         group_sync<kBulkConsumers>(0);
     }
     if (bad) atomicOr(A.ovf, 1);
@@ -956,7 +977,7 @@ static int launch_astep_cfg(const AStepArgs &A0, void *stream) {
     // (only where the eMA is a real share of the step: >= 0.05 split terms per gathered
     // byte; gather-dominated GENERAL steps such as u14-2's 13 = 5 + 8 (0.011) run one row
     // per group so the gathers of different rows overlap)
-    const bool multi = A.comb == COMB_GENERAL && !A.top && A.nterms >= 8 && gt >= 32 && tune != 5 &&
+    const bool multi = A.comb == COMB_GENERAL && !A.top && A.nterms >= 8 && gt >= 32 && tune != 5 && !A.b_out &&
                        (A.terms_per_byte >= vtpb || tune == 9) &&
                        (size_t)(256 / gt) * 4 * A.smem_group * sizeof(T) <= 200 * 1024;
     // wide gather rows without V-row batching: bulk-staged loads (SG2V_BULK=0 disables,
@@ -980,7 +1001,7 @@ static int launch_astep_cfg(const AStepArgs &A0, void *stream) {
     // (SG2V_HEAVY=0 disables)
     static int heavy = -1;
     if (heavy < 0) { const char *e = getenv("SG2V_HEAVY"); heavy = e ? atoi(e) : 1; }
-    if (MODE == 0 && heavy && !multi && !A.src_hist && A.pmap != nullptr && gt < 256 && nvec <= 32 &&
+    if (MODE == 0 && heavy && !multi && !A.b_out && !A.src_hist && A.pmap != nullptr && gt < 256 && nvec <= 32 &&
         A.n_heavy > 0 && A.n_heavy < A.n) {
         AStepArgs H = A;
         H.n = A.n_heavy;
@@ -1100,6 +1121,8 @@ int launch_astep_vp(const Graph &g, const Plan &pl, const Step &st, const uint8_
     A.bg = nullptr;
     A.ovf = ovf;
     A.n_heavy = g.n_deg_ge[kHeavyLog2];
+    A.b_out = nullptr;
+    A.bg_pos = 0;
     // stage M_a next to B only while both fit comfortably (occupancy); else L1
     A.aoff = st.self_a ? 0 : st.ldb;
     static int stage_kb = -1;  // SG2V_STAGE_KB (experiments): M_a staging threshold
@@ -1107,7 +1130,7 @@ int launch_astep_vp(const Graph &g, const Plan &pl, const Step &st, const uint8_
     A.stage_a = (st.comb == COMB_GENERAL) && (st.self_a || (st.ldb + st.lda) * pl.elem <= (int64_t)stage_kb * 1024);
     A.tpo = 1;  // set per launch configuration (launch_astep_cfg)
     A.smem_group = st.ldb + (A.stage_a && !st.self_a ? st.lda : 0);
-    A.tagged = g.n < (int64_t(1) << kClassShift);
+    A.tagged = std::max(g.n, pl.n_rows) < (int64_t(1) << kClassShift);  // as bucket_kernel tagged (full n)
     {
         // rows of the hottest H neighbours fit in ~75 MB of the 126 MB L2
         static int64_t l2 = 0;
@@ -1144,11 +1167,20 @@ int launch_astep_vp(const Graph &g, const Plan &pl, const Step &st, const uint8_
         A.src_hist = 0;
     } else if (vp && vp->mode == 3) {  // fused step, whole rows from the staging buffer
         A.hint = 0;
+    } else if (vp && vp->mode == 4) {  // split pipeline, gather half: B rows -> bg by position
+        A.b_out = vp->bg;
+        A.stage_a = 0;
+        A.smem_group = st.ldb;
+    } else if (vp && vp->mode == 5) {  // split pipeline, eMA half: B rows from bg by position
+        A.bsrc_global = 1;
+        A.bg = vp->bg;
+        A.bg_pos = 1;
+        A.src_hist = 0;
     }
     int cls = st.top ? 3 : 2;
     prof_begin(cls, stream);
     int rc;
-    const int md = vp && vp->mode != 3 ? vp->mode : 0;
+    const int md = !vp ? 0 : vp->mode == 3 || vp->mode == 4 ? 0 : vp->mode == 5 ? 2 : vp->mode;
     if (pl.prec == SG2V_F32)
         rc = md == 1 ? launch_astep_cfg<float, double, 1>(A, stream)
                      : md == 2 ? launch_astep_cfg<float, double, 2>(A, stream) : launch_astep_cfg<float, double, 0>(A, stream);
@@ -1159,11 +1191,59 @@ int launch_astep_vp(const Graph &g, const Plan &pl, const Step &st, const uint8_
         rc = md == 1 ? launch_astep_cfg<u64, u64, 1>(A, stream)
                      : md == 2 ? launch_astep_cfg<u64, u64, 2>(A, stream) : launch_astep_cfg<u64, u64, 0>(A, stream);
     // algorithmic bytes of a column tile: its share of the step's gather
-    const double tile_frac = (!vp || vp->mode == 3) ? 1.0
-                             : (vp->mode == 1 ? (double)vp->cnt / (double)std::max<int64_t>(st.cp, 1) : 0.0);
-    prof_end(cls, st.alg_bytes * tile_frac, stream, st.impl_bytes * tile_frac,
-             !vp || vp->mode >= 2 ? st.ema_terms : 0.0);
+    // profile records: a column tile carries its share of the gather; a split-pipeline
+    // chunk carries its share of the step (gather bytes on the gather launch, eMA terms
+    // on the eMA launch)
+    const double rows_frac = (double)g.n / (double)std::max<int64_t>(pl.n_rows, 1);
+    double fb = 1.0, ft = 1.0;
+    if (vp && vp->mode == 1) { fb = (double)vp->cnt / (double)std::max<int64_t>(st.cp, 1); ft = 0.0; }
+    else if (vp && vp->mode == 2) { fb = 0.0; }
+    else if (vp && vp->mode == 4) { fb = rows_frac; ft = 0.0; }
+    else if (vp && vp->mode == 5) { fb = 0.0; ft = rows_frac; }
+    prof_end(cls, st.alg_bytes * fb, stream, st.impl_bytes * fb, st.ema_terms * ft);
     return rc;
+}
+
+// ---------------------------------------------------------------------------
+// split eMA pipeline (GENERAL eMA-heavy steps, Step::split_ema): the rows (degree
+// order) are cut into chunks of sp.rows; chunk c's gather (bulk / register kernel, B
+// rows to bg[c % 2]) runs on the main stream while chunk c-1's eMA (MODE 2 combine,
+// V interleaved rows) runs on the aux stream, so the HBM-bound gather and the
+// shared-memory-bound eMA of different rows overlap on the SMs (one kernel of each
+// kind co-resident per SM) instead of alternating inside one CTA.
+// ---------------------------------------------------------------------------
+int launch_astep_split(const Graph &g, const Plan &pl, const Step &st, const uint8_t *colors, const int32_t *hcnt,
+                       const int32_t *bcol, char *tables, void *rowval, int *ovf, void *stream, const SplitCtx &sp) {
+    cudaStream_t s0 = (cudaStream_t)stream, s1 = (cudaStream_t)sp.aux;
+    const int64_t nchunks = (g.n + sp.rows - 1) / sp.rows;
+    const size_t half = (size_t)sp.rows * st.ldb * pl.elem;
+    cudaError_t e;
+    if ((e = cudaEventRecord(sp.ready[0], s0))) return (int)e;  // aux must see the previous steps
+    if ((e = cudaStreamWaitEvent(s1, sp.ready[0], 0))) return (int)e;
+    for (int64_t c = 0; c < nchunks; ++c) {
+        const int par = (int)(c & 1);
+        const int64_t r0 = c * sp.rows, r1 = std::min<int64_t>(g.n, r0 + sp.rows);
+        if (c >= 2 && (e = cudaStreamWaitEvent(s0, sp.done[par], 0))) return (int)e;  // bg[par] consumed
+        Graph gc = g;  // rows r0..r1 of the degree order
+        gc.d_order = g.d_order + r0;
+        gc.n = r1 - r0;
+        gc.n_deg_ge[kHeavyLog2] = std::max<int64_t>(0, std::min<int64_t>(g.n_deg_ge[kHeavyLog2], r1) - r0);
+        VpArgs va;
+        va.mode = 4;  // gather only -> bg
+        va.bg = sp.bg + par * half;
+        int rc = launch_astep_vp(gc, pl, st, colors, hcnt, bcol, tables, rowval, ovf, s0, &va);
+        if (rc) return rc;
+        if ((e = cudaEventRecord(sp.ready[par], s0))) return (int)e;
+        if ((e = cudaStreamWaitEvent(s1, sp.ready[par], 0))) return (int)e;
+        va.mode = 5;  // eMA from bg (by position)
+        rc = launch_astep_vp(gc, pl, st, colors, hcnt, bcol, tables, rowval, ovf, s1, &va);
+        if (rc) return rc;
+        if ((e = cudaEventRecord(sp.done[par], s1))) return (int)e;
+    }
+    // join: the main stream continues after every eMA chunk
+    for (int par = 0; par < 2 && par < nchunks; ++par)
+        if ((e = cudaStreamWaitEvent(s0, sp.done[par], 0))) return (int)e;
+    return 0;
 }
 
 // ---------------------------------------------------------------------------

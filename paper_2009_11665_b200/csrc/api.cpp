@@ -407,7 +407,7 @@ namespace sg2v {
 // is exactly the plan's own layout (Plan::ws_bytes).
 struct BatchLayout {
     int64_t off_colors = 0, off_hist = 0, off_hcnt = 0, off_bcol = 0, off_rowval = 0, off_partial = 0,
-            off_results = 0, off_flag = 0, bytes = 0;
+            off_results = 0, off_flag = 0, off_split = 0, bytes = 0;
 };
 
 static int64_t rup(int64_t x, int64_t m) { return (x + m - 1) / m * m; }
@@ -431,6 +431,9 @@ static BatchLayout batch_layout(const std::vector<Plan *> &pls, int64_t n, int64
     L.off_partial = off; off = rup(off + kReduceBlocks * 8, 256);
     L.off_results = off; off = rup(off + (int64_t)kResultsRing * 8 * (int64_t)std::max<size_t>(pls.size(), 1), 256);
     L.off_flag = off;    off = rup(off + 16, 256);
+    int64_t split = 0;
+    for (Plan *p : pls) split = std::max(split, p->split_bytes);
+    L.off_split = off;   off = rup(off + split, 256);
     L.bytes = off;
     return L;
 }
@@ -863,6 +866,33 @@ static sg2v_status count_core(const sg2v_graph *g, const sg2v_template *const *t
         int32_t *hcnt = (int32_t *)(ws + L.off_hcnt);
         int32_t *bcol = (int32_t *)(ws + L.off_bcol);
         int *dflag = (int *)(ws + L.off_flag);
+        // split eMA pipeline: an aux stream + events when some step uses it (SG2V_SPLIT=0 off)
+        static int split_on = -1;
+        if (split_on < 0) { const char *e = getenv("SG2V_SPLIT"); split_on = e ? atoi(e) : 1; }
+        SplitCtx sp;
+        struct SplitFree {
+            SplitCtx &c;
+            ~SplitFree() {
+                for (int q = 0; q < 2; ++q) {
+                    if (c.ready[q]) cudaEventDestroy(c.ready[q]);
+                    if (c.done[q]) cudaEventDestroy(c.done[q]);
+                }
+                if (c.aux) cudaStreamDestroy((cudaStream_t)c.aux);
+            }
+        } split_free{sp};
+        bool any_split = false;
+        for (Plan *p : pls)
+            for (const Step &stp : p->steps) any_split = any_split || (stp.split_ema && split_on);
+        if (any_split) {
+            cudaStream_t aux;
+            SG2V_CK(cudaStreamCreateWithFlags(&aux, cudaStreamNonBlocking));
+            sp.aux = aux;
+            for (int q = 0; q < 2; ++q) {
+                SG2V_CK(cudaEventCreateWithFlags(&sp.ready[q], cudaEventDisableTiming));
+                SG2V_CK(cudaEventCreateWithFlags(&sp.done[q], cudaEventDisableTiming));
+            }
+            sp.bg = ws + L.off_split;
+        }
         const bool anch = pls[0]->layout == LAYOUT_ANCHORED;
         bool need_hist = false;
         for (Plan *p : pls) need_hist = need_hist || p->need_hist;
@@ -878,8 +908,13 @@ static sg2v_status count_core(const sg2v_graph *g, const sg2v_template *const *t
             for (int32_t tq = 0; tq < m; ++tq) {
                 const Plan *pl = pls.size() > 1 ? &J.views[tq] : pls[tq];
                 for (const Step &stp : pl->steps) {
-                    rc = anch ? launch_astep(*g, *pl, stp, colors, hcnt, bcol, ws, rowval, dflag, s)
-                              : launch_step(*g, *pl, stp, colors, H, ws, rowval, dflag, s);
+                    if (anch && stp.split_ema && sp.aux) {
+                        sp.rows = pl->split_rows;
+                        rc = launch_astep_split(*g, *pl, stp, colors, hcnt, bcol, ws, rowval, dflag, s, sp);
+                    } else {
+                        rc = anch ? launch_astep(*g, *pl, stp, colors, hcnt, bcol, ws, rowval, dflag, s)
+                                  : launch_step(*g, *pl, stp, colors, H, ws, rowval, dflag, s);
+                    }
                     if (rc == -1) {
                         set_error("row too wide for on-chip B (shared memory > 227 KB)");
                         return SG2V_ENOMEM;

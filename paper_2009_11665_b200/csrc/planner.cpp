@@ -549,6 +549,13 @@ static bool plan_chain(const Template &t, const Chain &c, int root, int64_t n, i
             }
             st.alg_bytes = u;
         }
+        {
+            // eMA-heavy GENERAL steps with wide gather rows run as the split two-stream
+            // pipeline (launch_astep_split): same terms-per-byte test as the V-row eMA
+            const int64_t nvec_p = (st.proj_p ? st.ldseg_p : st.ldp) / vn;
+            st.split_ema = anch && st.comb == COMB_GENERAL && !st.top && st.src == SRC_GATHER && st.nterms >= 8 &&
+                           st.ema_terms >= 0.05 * bytes && nvec_p >= 64;
+        }
         st.gt = pick_gt(std::max({st.ldp, st.ldb, st.lds, st.comb == COMB_GENERAL ? st.lda : 0}), vn);
         model += mbytes / kHbm + st.ema_terms / kTermRate;
         alg_total += st.alg_bytes;
@@ -574,6 +581,15 @@ static bool plan_chain(const Template &t, const Chain &c, int root, int64_t n, i
     pl.model_time = model;
     pl.alg_bytes_total = alg_total;
 
+    // split eMA pipeline buffers: two chunks of B rows
+    pl.n_rows = n;
+    {
+        int64_t ldb = 0;
+        for (const Step &st : pl.steps)
+            if (st.split_ema) ldb = std::max(ldb, st.ldb);
+        pl.split_rows = ldb ? std::min<int64_t>(n, std::max<int64_t>(1024, (n + 15) / 16)) : 0;
+        pl.split_bytes = 2 * pl.split_rows * ldb * pl.elem;
+    }
     // workspace layout
     int64_t off = pl.tables_bytes;
     pl.off_colors = off;  off = round_up(off + std::max<int64_t>(n, 1) + 16, 256);
@@ -584,6 +600,7 @@ static bool plan_chain(const Template &t, const Chain &c, int root, int64_t n, i
     pl.off_partial = off; off = round_up(off + kReduceBlocks * 8, 256);
     pl.off_results = off; off = round_up(off + kResultsRing * 8, 256);
     pl.off_flag = off;    off = round_up(off + 16, 256);
+    pl.off_split = off;   off = round_up(off + pl.split_bytes, 256);
     pl.ws_bytes = off;
     return true;
 }
@@ -913,7 +930,7 @@ std::string Plan::describe() const {
           << ",\"comb\":\"" << (s.comb == COMB_ACTIVE_LEAF ? "active_leaf" : "general") << "\""
           << ",\"cs\":" << s.cs << ",\"ca\":" << s.ca << ",\"cp\":" << s.cp
           << ",\"cb\":" << s.cb << ",\"lds\":" << s.lds << ",\"ldp\":" << s.ldp << ",\"nterms\":" << s.nterms
-          << ",\"self\":" << (s.self_a ? "true" : "false")
+          << ",\"self\":" << (s.self_a ? "true" : "false") << ",\"split_ema\":" << (s.split_ema ? "true" : "false")
           << ",\"proj_out\":" << (s.proj_out ? "true" : "false") << ",\"proj_p\":" << (s.proj_p ? "true" : "false")
           << ",\"plain_out\":" << (s.plain_out ? "true" : "false") << ",\"ldsx\":" << s.ldsx
  << ",\"gt\":" << s.gt << ",\"alg_bytes\":" << s.alg_bytes << ",\"impl_bytes\":" << s.impl_bytes

@@ -2,6 +2,8 @@
 // the kernel launchers of libsg2v.so.  Nothing here is visible through the ABI.
 #pragma once
 
+#include <cuda_runtime.h>
+
 #include <cstddef>
 #include <cstdint>
 #include <map>
@@ -43,7 +45,8 @@ struct Graph {
 // Column tile / combine descriptor of a vertex-partitioned step.
 struct VpArgs {
     int mode = 0;               // 1 = tile gather into bg, 2 = combine from bg,
-                                // 3 = fused step gathering whole rows from `stage`
+                                // 3 = fused step gathering whole rows from `stage`,
+                                // 4/5 = split eMA pipeline: gather -> bg / eMA from bg (by position)
     const char *stage = nullptr;  // [n_global][stage_ld] all-gathered column tile
     int64_t stage_ld = 0, u0 = 0, cnt = 0;
     char *bg = nullptr;         // [n_local][ldb]
@@ -87,6 +90,7 @@ struct Step {
     int64_t omap_off = -1;                 // projected output: write map (int32 offset)
     std::string canon_out, canon_a, canon_p;  // rooted classes of T_s, T_a, T_p (table sharing)
     int gt = 32;                           // threads per row group (step kernel)
+    bool split_ema = false;                // eMA-heavy GENERAL step: gather and eMA as a two-stream pipeline
     double alg_bytes = 0.0;                // algorithmic HBM bytes of the METHOD:
                                            //   useful gather + CSR + M_a + plain-width output (layout-independent)
     double impl_bytes = 0.0;               // compulsory bytes of the implemented layout (plain-width gathers
@@ -120,6 +124,8 @@ struct Plan {
     int64_t n_global = 0, tile_w = 0;      // tile width in elements (multiple of 16 B)
     int64_t off_stage = 0, off_send = 0, off_bg = 0, off_colors_g = 0, off_part = 0;
     int64_t ws_bytes = 0;
+    int64_t n_rows = 0;                    // rows the plan was made for (n)
+    int64_t split_rows = 0, split_bytes = 0, off_split = 0;  // split eMA pipeline: chunk rows, 2 B buffers
     std::vector<int32_t> index;   // concatenated index tables (host copy)
     int32_t *d_index = nullptr;   // device copy (owned by the template's cache)
     int top_leaf_col_off = -1;    // idx offset of topcol[k] when the top step is leaf-active
@@ -173,6 +179,15 @@ int launch_astep_vp(const Graph &g, const Plan &pl, const Step &st, const uint8_
 // F32 overflow flag of one sg2v_count call: a device int inside its workspace
 int ovf_reset(int *dflag, void *stream);
 int ovf_read(const int *dflag, int *flag, void *stream);
+// split eMA pipeline context (count_core): aux stream, events, the two B-row buffers
+struct SplitCtx {
+    void *aux = nullptr;
+    cudaEvent_t ready[2] = {nullptr, nullptr}, done[2] = {nullptr, nullptr};
+    char *bg = nullptr;
+    int64_t rows = 0;
+};
+int launch_astep_split(const Graph &g, const Plan &pl, const Step &st, const uint8_t *colors, const int32_t *hcnt,
+                       const int32_t *bcol, char *tables, void *rowval, int *ovf, void *stream, const SplitCtx &sp);
 int launch_pack_tile(int64_t n, const char *src, int64_t ld_bytes, int64_t u0_bytes, int64_t w_bytes, char *dst,
                      int64_t dst_ld_bytes, void *stream);
 int launch_bg_rowval(const Plan &pl, int64_t n, const char *bg, int64_t ldb, void *rowval, void *stream);

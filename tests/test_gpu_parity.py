@@ -367,3 +367,16 @@ def test_shared_and_self_steps_vs_oracle(oracle, name):
     d = sg.plan_describe(G := _load(g), T, "u64")
     assert len(d["steps"]) < k - 1 or any(s.get("self") for s in d["steps"]) or name == "caterpillar"
     _check_all(oracle, g, e, [(3, 0), (3, 1)], roots=tuple(range(-1, k)), precs=("u64",))
+
+
+def test_split_ema_pipeline(oracle):
+    """eMA-heavy GENERAL steps run as the two-stream split pipeline (gather of row chunk c
+    beside the eMA of chunk c-1, B rows handed over in HBM): per-vertex values equal the
+    oracle's with several chunks (n = 5000 -> 1024-row chunks), U64 exact and F32 1e-4."""
+    g = erdos_renyi(5000, 25_000, seed=21)
+    G = _load(g)
+    for name in ("u13-2", "u14-2"):
+        e = TEMPLATES[name]
+        d = sg.plan_describe(G, sg.template_build(_k(e), e), "u64")
+        assert any(s["split_ema"] for s in d["steps"]), name
+        _check_all(oracle, g, e, [(4, 1)], precs=("u64", "f32"), layouts=("anchored",))
