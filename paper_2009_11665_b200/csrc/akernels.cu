@@ -262,8 +262,10 @@ __device__ __forceinline__ void gather_row(const AStepArgs &A, int64_t i, int ci
                 for (int q = 0; q < R; ++q) {
                     if (need[q]) {
 #pragma unroll
-                        for (int el = 0; el < VN; ++el)
-                            if (tt[q][el] >= 0) sB[(size_t)tt[q][el] * STRIDE] += vget<T>(acc[q], el);
+                        for (int el = 0; el < VN; ++el)  // (u < cp: a column tile's last vector
+                                                          //  may run into the next tile)
+                            if (tt[q][el] >= 0 && (v0 + q * GT + t) * VN + el < A.cp)
+                                sB[(size_t)tt[q][el] * STRIDE] += vget<T>(acc[q], el);
                     }
                 }
             }
@@ -629,7 +631,7 @@ __global__ void __launch_bounds__(256) astep_heavy_kernel(AStepArgs A) {
                     for (int g2 = 1; g2 < NG; ++g2) Vec<T>::add(sum, scratch[(size_t)g2 * SG * R + q * SG + ll]);
 #pragma unroll
                     for (int el = 0; el < VN; ++el)
-                        if (tt[el] >= 0) sB[tt[el]] += vget<T>(sum, el);
+                        if (tt[el] >= 0 && v * VN + el < A.cp) sB[tt[el]] += vget<T>(sum, el);
                 }
                 group_sync<256>(0);
             }
@@ -810,7 +812,7 @@ __global__ void __launch_bounds__(NC + 32, BulkMinBlocks<NC>::value) astep_bulk_
                 if (v < nvec_p) {
 #pragma unroll
                     for (int el = 0; el < VN; ++el)
-                        if (tt[q][el] >= 0) sB[tt[q][el]] += vget<T>(acc[q], el);
+                        if (tt[q][el] >= 0 && v * VN + el < A.cp) sB[tt[q][el]] += vget<T>(acc[q], el);
                 }
             }
             group_sync<kBulkConsumers>(0);  // colours x and x' may push to the same T
@@ -918,6 +920,10 @@ static int launch_astep_bulk_t(const AStepArgs &A, void *stream) {
                (size_t)s * stage_bytes;
     };
     while (S > 3 && smem_of(S) > 220 * 1024) --S;
+    // when the row (B + M_a) is so wide that a second CTA cannot fit on the SM, give the
+    // one CTA every stage that fits: bytes in flight per SM are what keep HBM busy
+    if (smem_of(S) > 110 * 1024)
+        while (S < 32 && smem_of(S + 1) <= 220 * 1024) ++S;
     const size_t smem = smem_of(S);
     if (smem > 227 * 1024) return -1;
     auto kern = astep_bulk_kernel<T, RT, R, NC>;

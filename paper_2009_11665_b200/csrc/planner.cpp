@@ -587,7 +587,9 @@ static bool plan_chain(const Template &t, const Chain &c, int root, int64_t n, i
         int64_t ldb = 0;
         for (const Step &st : pl.steps)
             if (st.split_ema) ldb = std::max(ldb, st.ldb);
-        pl.split_rows = ldb ? std::min<int64_t>(n, std::max<int64_t>(1024, (n + 15) / 16)) : 0;
+        // 32 chunks: the first chunk's gather (the hub rows) is the part the pipeline
+        // cannot hide, so it is kept short
+        pl.split_rows = ldb ? std::min<int64_t>(n, std::max<int64_t>(1024, (n + 31) / 32)) : 0;
         pl.split_bytes = 2 * pl.split_rows * ldb * pl.elem;
     }
     // workspace layout

@@ -135,3 +135,56 @@ def test_world2_callback_equals_single(oracle):
         for j in range(2):
             wf = oracle.count(g, k, e, oracle.colors(5, j, g.n, k), arith=oracle.ARITH_F64)[0]
             assert abs(out[0][name + "/f32"][j] - wf) <= 1e-4 * wf, name
+
+
+def _nccl_worker(rank, world, port, q):
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    torch.cuda.set_device(rank)
+    dist.init_process_group("nccl", rank=rank, world_size=world, device_id=torch.device("cuda", rank))
+    import paper_2009_11665_b200 as sgw
+    uid = [sgw.Comm.unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(uid, src=0)
+    comm = sgw.Comm.nccl(uid[0], rank, world)
+    g = rmat(12, 60_000, 0.45, 0.22, 0.22, seed=6)
+    b, nl, _, _ = _part(g, rank, world)
+    oon, ro2, ci2 = sgw.partition_relabel(g.row_offsets, g.col_indices, world)
+    Gr = sgw.graph_load_partition(g.n, b, nl, ro2[b:b + nl + 1] - ro2[b], ci2[ro2[b]:ro2[b + nl]])
+    sgw.graph_set_vertex_ids(Gr, oon)
+    res = {}
+    for name in ("u5-2", "u7-2", "u10-2"):
+        e = TEMPLATES[name]
+        T = sgw.template_build(_k(e), e)
+        _, c0 = sgw.count(Gr, T, n_iter=2, seed=5, precision="u64", comm=comm, col_tile=0)
+        _, c1 = sgw.count(Gr, T, n_iter=2, seed=5, precision="u64", comm=comm, col_tile=16)
+        res[name] = ([int(x) for x in c0], [int(x) for x in c1])
+    comm.free()
+    dist.barrier()
+    dist.destroy_process_group()
+    q.put((rank, res))
+
+
+@pytest.mark.skipif(not torch.cuda.is_available() or torch.cuda.device_count() < 2,
+                    reason="needs two GPUs (NCCL over NVLink; runs on the 8-GPU node)")
+def test_world2_nccl_two_gpus(oracle):
+    """One process per GPU, NCCL all-gathers over NVLink, balanced relabelled
+    partition: whole-row exchange and column tiles both equal the oracle's counts."""
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_nccl_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    out = dict(q.get(timeout=600) for _ in procs)
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    g = rmat(12, 60_000, 0.45, 0.22, 0.22, seed=6)
+    for name in ("u5-2", "u7-2", "u10-2"):
+        e = TEMPLATES[name]
+        k = _k(e)
+        want = [oracle.count(g, k, e, oracle.colors(5, j, g.n, k)) for j in range(2)]
+        for r in (0, 1):
+            assert out[r][name][0] == want and out[r][name][1] == want, (name, r)
