@@ -302,28 +302,43 @@ def roofline(args, prof, recs, plan):
         L = len(cols[0])
         same = [c for c in cols if len(c) == L]
         names = ["color", "bucket" if args.layout != "dense" else "hist"]
+        nch = -(-plan.get("n_rows", 0) // plan["split_rows"]) if plan.get("split_rows") else 0
         for st in plan["steps"]:
-            names.append(f"s={st['s']}={st['a']}+{st['p']}{' top' if st['top'] else ''}"
-                         f"{' self' if st.get('self') else ''}")
+            nm = (f"s={st['s']}={st['a']}+{st['p']}{' top' if st['top'] else ''}"
+                  f"{' self' if st.get('self') else ''}")
+            if st.get("split_ema") and nch:  # split pipeline: a gather and an eMA launch per chunk
+                names += [nm + " (split: gather)", nm + " (split: eMA)"] * nch
+            else:
+                names.append(nm)
         names.append("reduce")
+        agg = {}
         for q in range(L):
-            ms_q = statistics.mean(c[q]["ms"] for c in same)
-            a_q, i_q = same[0][q]["alg_bytes"], same[0][q]["impl_bytes"]
-            steps_tab.append({"launch": names[q] if len(names) == L else same[0][q]["cls"], "ms": ms_q,
-                              "alg_GB": a_q / 1e9, "impl_GB": i_q / 1e9,
-                              "alg_frac": a_q / (ms_q / 1e3) / 1e9 / peak if ms_q > 0 else None})
+            nm = names[q] if len(names) == L else same[0][q]["cls"] + f"#{q}"
+            a = agg.setdefault(nm, {"launch": nm, "ms": 0.0, "alg_GB": 0.0, "impl_GB": 0.0, "ema_terms": 0.0,
+                                    "launches": 0})
+            a["ms"] += statistics.mean(c[q]["ms"] for c in same)
+            a["alg_GB"] += same[0][q]["alg_bytes"] / 1e9
+            a["impl_GB"] += same[0][q]["impl_bytes"] / 1e9
+            a["ema_terms"] += same[0][q]["ema_terms"]
+            a["launches"] += 1
+        for a in agg.values():
+            a["alg_frac"] = a["alg_GB"] / a["ms"] / peak if a["ms"] > 0 and a["alg_GB"] > 0 else None
+            if a["ema_terms"] > 0 and a["ms"] > 0:
+                a["ema_terms_per_s"] = a["ema_terms"] / (a["ms"] / 1e3)
+            steps_tab.append(a)
     ema = None
-    gen = [r for r in recs if r["ema_terms"] > 0]
+    gen = [a for a in steps_tab if a.get("ema_terms_per_s")]
     if gen:
-        t_ms = sum(r["ms"] for r in gen)
-        terms = sum(r["ema_terms"] for r in gen)
         smem_roof = 148 * SMEM_B_PER_CLK_SM * sm_mhz * 1e6 / (2 * plan["elem"])
         fma_roof = 148 * FMA_PER_CLK_SM * sm_mhz * 1e6
-        rate = terms / (t_ms / 1e3) if t_ms > 0 else 0.0
-        ema = {"terms_per_colouring": terms / max(len(cols), 1), "ms_per_colouring": t_ms / max(len(cols), 1),
+        top = max(gen, key=lambda a: a["ema_terms"])
+        rate = top["ema_terms_per_s"]
+        ema = {"step": top["launch"], "terms_per_colouring": top["ema_terms"], "ms_per_colouring": top["ms"],
                "terms_per_s": rate, "smem_roof_terms_per_s": smem_roof, "frac_smem": rate / smem_roof,
                "fma_roof_per_s": fma_roof, "frac_fma": rate / fma_roof,
-               "note": "time of the GENERAL launches (gather included): a lower bound on the eMA rate"}
+               "note": "the GENERAL step with the most split terms; its eMA launches' CUDA-event time (split "
+                       "pipeline: the eMA launches alone; fused: gather included, a lower bound on the eMA rate). "
+                       "smem roof = 148 SMs x 128 B/clk x SM clock / (2 operands x element bytes)"}
     return rf, steps_tab, ema
 
 

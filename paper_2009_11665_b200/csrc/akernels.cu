@@ -45,41 +45,54 @@ __global__ void __launch_bounds__(256) bucket_kernel(int64_t n, int k, int kp, c
                                                      const uint8_t *__restrict__ vclass,
                                                      int32_t *__restrict__ hcnt, int32_t *__restrict__ bcol,
                                                      int64_t row_begin) {
-    // rows are local (row_begin + i is the global id); neighbour ids are global
+    // rows are local (row_begin + i is the global id); neighbour ids are global.
+    // Per warp-row: pass 1 counts colours (lanes of equal colour found by match_any, the
+    // lowest lane adds the group size to the warp's shared counter: integer, exact);
+    // pass 2 writes each neighbour at its colour bucket's running position + its rank
+    // among equal-colour lanes of the chunk (stable within a colour).
+    __shared__ int cnt_s[8][32];
     const bool tag = vclass != nullptr && n < (int64_t(1) << kClassShift);
-    const int lane = threadIdx.x & 31;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    int *cnt = cnt_s[w];
     const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
-    for (int64_t i = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); i < n; i += warps) {
+    for (int64_t i = blockIdx.x * (int64_t)(blockDim.x >> 5) + w; i < n; i += warps) {
         const int64_t e0 = rowptr[i], e1 = rowptr[i + 1];
-        int cnt = 0;  // lane x: neighbours of colour x
-        for (int64_t base = e0; base < e1; base += 32) {
-            const int64_t e = base + lane;
-            const int c = (e < e1) ? (int)colors[__ldg(col + e)] : 255;
-            for (int x = 0; x < k; ++x) {
-                const unsigned b = __ballot_sync(0xffffffffu, c == x);
-                if (lane == x) cnt += __popc(b);
-            }
+        cnt[lane] = 0;
+        __syncwarp();
+        // pass 1 (two chunks in flight)
+        for (int64_t base = e0; base < e1; base += 64) {
+            const int64_t ea = base + lane, eb = base + 32 + lane;
+            const int32_t ja = ea < e1 ? __ldg(col + ea) : -1, jb = eb < e1 ? __ldg(col + eb) : -1;
+            const int ca = ja >= 0 ? (int)colors[ja] : 255, cb = jb >= 0 ? (int)colors[jb] : 255;
+            const unsigned ma = __match_any_sync(0xffffffffu, ca), mb = __match_any_sync(0xffffffffu, cb);
+            if (ca != 255 && (__ffs(ma) - 1) == lane) atomicAdd(&cnt[ca], __popc(ma));
+            if (cb != 255 && (__ffs(mb) - 1) == lane) atomicAdd(&cnt[cb], __popc(mb));
         }
-        if (lane < kp) hcnt[i * kp + lane] = (lane < k) ? cnt : 0;
+        __syncwarp();
+        const int mine = lane < k ? cnt[lane] : 0;
+        if (lane < kp) hcnt[i * kp + lane] = mine;
         // exclusive scan over colours -> start of each colour's bucket
-        int incl = (lane < k) ? cnt : 0;
+        int incl = mine;
 #pragma unroll
         for (int off = 1; off < 32; off <<= 1) {
             const int y = __shfl_up_sync(0xffffffffu, incl, off);
             if (lane >= off) incl += y;
         }
-        int run = incl - ((lane < k) ? cnt : 0);
+        __syncwarp();
+        cnt[lane] = incl - mine;  // running write position per colour
+        __syncwarp();
         for (int64_t base = e0; base < e1; base += 32) {
             const int64_t e = base + lane;
             const int32_t j = (e < e1) ? __ldg(col + e) : 0;
             const int c = (e < e1) ? (int)colors[j] : 255;
             const unsigned m = __match_any_sync(0xffffffffu, c);
-            const int pos = __shfl_sync(0xffffffffu, run, c & 31) + __popc(m & lanemask_lt());
-            if (e < e1) bcol[e0 + pos] = tag ? (j | ((int32_t)min((int)vclass[j], 31) << kClassShift)) : j;
-            for (int x = 0; x < k; ++x) {
-                const unsigned b = __ballot_sync(0xffffffffu, c == x);
-                if (lane == x) run += __popc(b);
+            if (e < e1) {
+                const int pos = cnt[c] + __popc(m & lanemask_lt());
+                bcol[e0 + pos] = tag ? (j | ((int32_t)min((int)vclass[j], 31) << kClassShift)) : j;
             }
+            __syncwarp();
+            if (e < e1 && (__ffs(m) - 1) == lane) cnt[c] += __popc(m);
+            __syncwarp();
         }
     }
 }
@@ -920,10 +933,10 @@ static int launch_astep_bulk_t(const AStepArgs &A, void *stream) {
                (size_t)s * stage_bytes;
     };
     while (S > 3 && smem_of(S) > 220 * 1024) --S;
-    // when the row (B + M_a) is so wide that a second CTA cannot fit on the SM, give the
-    // one CTA every stage that fits: bytes in flight per SM are what keep HBM busy
-    if (smem_of(S) > 110 * 1024)
-        while (S < 32 && smem_of(S + 1) <= 220 * 1024) ++S;
+    // one CTA per SM (B + M_a rows too wide for two): the register gather keeps more
+    // loads in flight there (u17 16 = 10 + 6: 0.88 s vs 1.10 s bulk, 1.30 s bulk with
+    // every stage that fits) -> caller falls back
+    if (smem_of(3) > 110 * 1024) return -2;
     const size_t smem = smem_of(S);
     if (smem > 227 * 1024) return -1;
     auto kern = astep_bulk_kernel<T, RT, R, NC>;
@@ -996,12 +1009,14 @@ static int launch_astep_cfg(const AStepArgs &A0, void *stream) {
         bulk_min = m ? atoi(m) : 64;
     }
     if (MODE == 0 && bulk && !multi && !A.src_hist && A.pmap != nullptr && nvec >= bulk_min && nvec <= 2048) {
-        if (nvec <= 64) return launch_astep_bulk_t<T, RT, 1, 64>(A, stream);
-        if (nvec <= 128) return launch_astep_bulk_t<T, RT, 1, 128>(A, stream);
-        if (nvec <= 256) return launch_astep_bulk_t<T, RT, 1, 256>(A, stream);
-        if (nvec <= 512) return launch_astep_bulk_t<T, RT, 2, 256>(A, stream);
-        if (nvec <= 1024) return launch_astep_bulk_t<T, RT, 4, 256>(A, stream);
-        return launch_astep_bulk_t<T, RT, 8, 256>(A, stream);
+        int rc;
+        if (nvec <= 64) rc = launch_astep_bulk_t<T, RT, 1, 64>(A, stream);
+        else if (nvec <= 128) rc = launch_astep_bulk_t<T, RT, 1, 128>(A, stream);
+        else if (nvec <= 256) rc = launch_astep_bulk_t<T, RT, 1, 256>(A, stream);
+        else if (nvec <= 512) rc = launch_astep_bulk_t<T, RT, 2, 256>(A, stream);
+        else if (nvec <= 1024) rc = launch_astep_bulk_t<T, RT, 4, 256>(A, stream);
+        else rc = launch_astep_bulk_t<T, RT, 8, 256>(A, stream);
+        if (rc != -2) return rc;  // -2: not a bulk configuration, register gather below
     }
     // heavy rows of narrow register-gather steps: CTA per row first, the rest after
     // (SG2V_HEAVY=0 disables)

@@ -923,7 +923,8 @@ std::string Plan::describe() const {
       << ",\"need_hist\":" << (need_hist ? "true" : "false") << ",\"hist_bytes\":" << hist_bytes
       << ",\"tables_bytes\":" << tables_bytes << ",\"workspace_bytes\":" << ws_bytes
       << ",\"model_seconds\":" << model_time << ",\"alg_bytes\":" << alg_bytes_total
-      << ",\"impl_bytes\":" << impl_bytes_total << ",\"steps\":[";
+      << ",\"impl_bytes\":" << impl_bytes_total << ",\"n_rows\":" << n_rows << ",\"split_rows\":" << split_rows
+      << ",\"steps\":[";
     for (size_t i = 0; i < steps.size(); ++i) {
         const Step &s = steps[i];
         o << (i ? "," : "") << "{\"s\":" << s.s << ",\"a\":" << s.a << ",\"p\":" << s.p
