@@ -322,7 +322,7 @@ def roofline(args, prof, recs, plan):
             a["ema_terms"] += same[0][q]["ema_terms"]
             a["launches"] += 1
         for a in agg.values():
-            a["alg_frac"] = a["alg_GB"] / a["ms"] / peak if a["ms"] > 0 and a["alg_GB"] > 0 else None
+            a["alg_frac"] = a["alg_GB"] / (a["ms"] / 1e3) / peak if a["ms"] > 0 and a["alg_GB"] > 0 else None
             if a["ema_terms"] > 0 and a["ms"] > 0:
                 a["ema_terms_per_s"] = a["ema_terms"] / (a["ms"] / 1e3)
             steps_tab.append(a)
