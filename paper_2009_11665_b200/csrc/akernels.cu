@@ -696,14 +696,14 @@ static int launch_astep_heavy(const AStepArgs &A, int64_t nvec, void *stream) {
 // register budget, and a consumer spends ~6 instructions per 16-B vector instead of
 // the register-gather's index/policy/address work per neighbour.
 // ---------------------------------------------------------------------------
-// NC consumer threads (64 .. 256 in whole warps, sized to the row) + one producer warp.
+// NC consumer threads (64, 128 or 256: sized to the row) + one producer warp.
 template <int NC>
 struct BulkMinBlocks {
-    static constexpr int value = NC >= 192 ? 3 : NC >= 96 ? 5 : 8;
+    static constexpr int value = NC == 256 ? 3 : NC == 128 ? 5 : 8;
 };
 
 template <typename T, typename RT, int R, int NC>
-__global__ void __launch_bounds__(NC + 32, BulkMinBlocks<NC>::value) astep_bulk_kernel(AStepArgs A, int S, uint32_t stage_bytes, int NB) {
+__global__ void __launch_bounds__(NC + 32, BulkMinBlocks<NC>::value) astep_bulk_kernel(AStepArgs A, int S, uint32_t stage_bytes) {
     constexpr int kBulkConsumers = NC;
     constexpr int VN = Vec<T>::N;
     constexpr int32_t kIdMask = (1 << kClassShift) - 1;
@@ -739,12 +739,8 @@ __global__ void __launch_bounds__(NC + 32, BulkMinBlocks<NC>::value) astep_bulk_
             const int64_t e0 = A.rowptr[i];
             // lane x holds this row's count of colour x
             const int hx = lane < k ? __ldg(A.hcnt + (size_t)i * A.kp + lane) : 0;
-            // live neighbours of the row (its own colour's bucket skipped): stages hold NB
-            // consecutive ones, the row's last stage possibly fewer
-            const int live = (int)(A.rowptr[i + 1] - e0) - __shfl_sync(0xffffffffu, hx, ci);
             int x = -1, left = 0;     // current colour bucket and its remaining neighbours
             int64_t e = e0;
-            int qn = 0;               // live neighbours issued in this row
             for (;;) {
                 // advance to the next non-empty bucket of a colour != ci (warp-uniform)
                 while (left == 0) {
@@ -759,23 +755,17 @@ __global__ void __launch_bounds__(NC + 32, BulkMinBlocks<NC>::value) astep_bulk_
                 const int32_t b = lane < take ? __ldg(A.bcol + e + lane) : 0;
                 const int rr = ci - (ci > x ? 1 : 0);
                 const int64_t sbase = A.ldseg_p > 0 ? (int64_t)rr * A.ldseg_p * (int64_t)sizeof(T) : 0;
-                for (int q = 0; q < take; ++q, ++qn) {
+                for (int q = 0; q < take; ++q) {
                     const int32_t bj = __shfl_sync(0xffffffffu, b, q);
-                    const int sub = qn % NB;
                     if (lane == 0) {
                         const int32_t j = A.tagged ? (bj & kIdMask) : bj;
                         const uint64_t pol = (A.tagged && (bj >> kClassShift) < A.hot_log2) ? pol_last : pol_first;
-                        if (sub == 0) {  // open a stage: its byte count first, then the copies
-                            const int nb = min(NB, live - qn);
-                            mbar_wait(empty + slot, ph ^ 1);
-                            mbar_arrive_expect_tx(full + slot, (uint32_t)nb * seg_bytes);
-                        }
-                        bulk_g2s(stages + (size_t)slot * stage_bytes + (size_t)sub * seg_bytes,
-                                 A.mp + (size_t)j * row_bytes + sbase, seg_bytes, full + slot, pol);
+                        mbar_wait(empty + slot, ph ^ 1);
+                        mbar_arrive_expect_tx(full + slot, seg_bytes);
+                        bulk_g2s(stages + (size_t)slot * stage_bytes, A.mp + (size_t)j * row_bytes + sbase, seg_bytes,
+                                 full + slot, pol);
                     }
-                    if (sub == NB - 1 || qn == live - 1) {
-                        if (++slot == S) { slot = 0; ph ^= 1; }
-                    }
+                    if (++slot == S) { slot = 0; ph ^= 1; }
                 }
                 e += take;
                 left -= take;
@@ -803,8 +793,6 @@ __global__ void __launch_bounds__(NC + 32, BulkMinBlocks<NC>::value) astep_bulk_
         }
         group_sync<kBulkConsumers>(0);
         const int32_t *h = A.hcnt + (size_t)i * A.kp;
-        const int live = (int)(A.rowptr[i + 1] - A.rowptr[i]) - __ldg(h + ci);
-        int qn = 0;  // live neighbours consumed in this row
         for (int x = 0; x < k; ++x) {
             const int cnt = __ldg(h + x);
             if (x == ci || cnt == 0) continue;
@@ -818,20 +806,17 @@ __global__ void __launch_bounds__(NC + 32, BulkMinBlocks<NC>::value) astep_bulk_
                 const int v = t + q * kBulkConsumers;
                 if (v < nvec_p) load_targets<T>(mp, v, tt[q]);
             }
-            for (int c = 0; c < cnt; ++c, ++qn) {
-                const int sub = qn % NB;
-                if (sub == 0) mbar_wait(full + slot, ph);
-                const unsigned char *st = stages + (size_t)slot * stage_bytes + (size_t)sub * seg_bytes;
+            for (int c = 0; c < cnt; ++c) {
+                mbar_wait(full + slot, ph);
+                const unsigned char *st = stages + (size_t)slot * stage_bytes;
 #pragma unroll
                 for (int q = 0; q < R; ++q) {
                     const int v = t + q * kBulkConsumers;
                     if (v < nvec_p) Vec<T>::add(acc[q], lds16(st + (size_t)v * 16));
                 }
-                if (sub == NB - 1 || qn == live - 1) {  // stage drained
-                    __syncwarp();
-                    if (lane == 0) mbar_arrive(empty + slot);
-                    if (++slot == S) { slot = 0; ph ^= 1; }
-                }
+                __syncwarp();
+                if (lane == 0) mbar_arrive(empty + slot);
+                if (++slot == S) { slot = 0; ph ^= 1; }
             }
             // push R_x into B: distinct targets within one colour
 #pragma unroll
@@ -938,12 +923,7 @@ static int launch_astep_bulk_t(const AStepArgs &A, void *stream) {
     constexpr int kBulkThreads = NC + 32;
     constexpr int VN = Vec<T>::N;
     const int64_t nvec_p = (A.ldseg_p > 0 ? A.ldseg_p : A.ldp) / VN;
-    // NB neighbour segments per stage (one mbarrier round trip per NB copies): ~4 KB stages
-    static int stage_kb = -1;  // SG2V_BULK_STAGE (experiments): target stage bytes, 0 = one segment
-    if (stage_kb < 0) { const char *e = getenv("SG2V_BULK_STAGE"); stage_kb = e ? atoi(e) : 4096; }
-    const int64_t seg = nvec_p * 16;
-    const int NB = (int)std::max<int64_t>(1, std::min<int64_t>(16, stage_kb > 0 ? stage_kb / seg : 1));
-    const uint32_t stage_bytes = (uint32_t)(((NB * seg) + 127) / 128 * 128);
+    const uint32_t stage_bytes = (uint32_t)(((nvec_p * 16) + 127) / 128 * 128);
     static int want_kb = -1;  // SG2V_BULK_KB (experiments): bulk bytes in flight per 256 consumers
     if (want_kb < 0) { const char *e = getenv("SG2V_BULK_KB"); want_kb = e ? atoi(e) : 48; }
     const int64_t kb = std::max<int64_t>(8, (int64_t)want_kb * NC / 256);
@@ -966,7 +946,7 @@ static int launch_astep_bulk_t(const AStepArgs &A, void *stream) {
     if (occ < 1) occ = 1;
     int64_t blocks = std::min<int64_t>(A.n, (int64_t)occ * num_sms());
     if (blocks < 1) blocks = 1;
-    kern<<<(unsigned)blocks, kBulkThreads, smem, (cudaStream_t)stream>>>(A, S, stage_bytes, NB);
+    kern<<<(unsigned)blocks, kBulkThreads, smem, (cudaStream_t)stream>>>(A, S, stage_bytes);
     return (int)cudaGetLastError();
 }
 
@@ -1030,11 +1010,8 @@ static int launch_astep_cfg(const AStepArgs &A0, void *stream) {
     }
     if (MODE == 0 && bulk && !multi && !A.src_hist && A.pmap != nullptr && nvec >= bulk_min && nvec <= 2048) {
         int rc;
-        // consumers sized to the row in whole warps (idle lanes still wait on every stage)
         if (nvec <= 64) rc = launch_astep_bulk_t<T, RT, 1, 64>(A, stream);
-        else if (nvec <= 96) rc = launch_astep_bulk_t<T, RT, 1, 96>(A, stream);
         else if (nvec <= 128) rc = launch_astep_bulk_t<T, RT, 1, 128>(A, stream);
-        else if (nvec <= 192) rc = launch_astep_bulk_t<T, RT, 1, 192>(A, stream);
         else if (nvec <= 256) rc = launch_astep_bulk_t<T, RT, 1, 256>(A, stream);
         else if (nvec <= 512) rc = launch_astep_bulk_t<T, RT, 2, 256>(A, stream);
         else if (nvec <= 1024) rc = launch_astep_bulk_t<T, RT, 4, 256>(A, stream);

@@ -32,8 +32,7 @@ KNOBS = [
     {"SG2V_VTPB": "0"}, {"SG2V_STAGE_KB": "0"}, {"SG2V_STAGE_KB": "4096"},
     {"SG2V_HINT": "0"}, {"SG2V_HOTFRAC": "0.00001"}, {"SG2V_HOTFRAC": "50"},
     {"SG2V_BULK": "0"}, {"SG2V_BULK_MIN": "1"}, {"SG2V_BULK_KB": "8"}, {"SG2V_HEAVY": "0"},
-    {"SG2V_EMA_SCHED": "1"}, {"SG2V_SPLIT": "0"}, {"SG2V_BULK_STAGE": "0"},
-    {"SG2V_BULK_MIN": "1", "SG2V_BULK_STAGE": "65536"},
+    {"SG2V_EMA_SCHED": "1"}, {"SG2V_SPLIT": "0"},
 ]
 
 _SCRIPT = r"""
