@@ -154,9 +154,13 @@ def cpu_sample(args, k, edges, full_n, full_nnz, steps=1, target_s=12.0):
     O.build()
     cores = O.get_threads()
     full_w = oracle_work(O, k, edges, full_n, full_nnz)
-    # pick the scale so one sample costs ~target_s (~4.5e8 u64 loop iterations/s/core, measured)
+    # pick the scale so one sample costs ~target_s (~4.5e8 u64 loop iterations/s/core, measured),
+    # but never below the scale whose widest oracle table is ~1 GB: small samples are cache- and
+    # overhead-dominated and extrapolate badly (scale 11: 2x the full-graph time, scale 14: 0.75x)
     rate = 4.5e8 * cores
     scale = 10
+    while scale < args.scale and _widest_table_gb(O, k, edges, 1 << scale) < 0.8:
+        scale += 1
     while scale < args.scale:
         n_s = 1 << (scale + 1)
         if full_w * n_s / full_n / rate > target_s:
