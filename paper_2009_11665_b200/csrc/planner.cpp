@@ -550,11 +550,12 @@ static bool plan_chain(const Template &t, const Chain &c, int root, int64_t n, i
             st.alg_bytes = u;
         }
         {
-            // eMA-heavy GENERAL steps with wide gather rows run as the split two-stream
-            // pipeline (launch_astep_split): same terms-per-byte test as the V-row eMA
+            // eMA-heavy GENERAL steps run as the split two-stream pipeline
+            // (launch_astep_split): same terms-per-byte test as the V-row eMA; gather rows of
+            // >= 16 vectors (narrower ones gain nothing from a separate gather launch)
             const int64_t nvec_p = (st.proj_p ? st.ldseg_p : st.ldp) / vn;
             st.split_ema = anch && st.comb == COMB_GENERAL && !st.top && st.src == SRC_GATHER && st.nterms >= 8 &&
-                           st.ema_terms >= 0.05 * bytes && nvec_p >= 64;
+                           st.ema_terms >= 0.05 * bytes && nvec_p >= 16;
         }
         st.gt = pick_gt(std::max({st.ldp, st.ldb, st.lds, st.comb == COMB_GENERAL ? st.lda : 0}), vn);
         model += mbytes / kHbm + st.ema_terms / kTermRate;
