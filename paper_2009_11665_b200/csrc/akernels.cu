@@ -38,13 +38,16 @@ __device__ __forceinline__ unsigned lanemask_lt() {
 // bcol entries carry the neighbour's degree-rank class in bits 26..30 when
 // n < 2^26 (the L2 residency hint of the gather; kClassShift), else bare ids.
 static constexpr int kClassShift = 26;
+// rows with >= 2^kHeavyLog2 neighbours (a prefix of the degree-descending order) are
+// walked by a whole CTA in the bucket, heavy-row and ring kernels
+static constexpr int kHeavyLog2 = 11;
 
 __global__ void __launch_bounds__(256) bucket_kernel(int64_t n, int k, int kp, const int64_t *__restrict__ rowptr,
                                                      const int32_t *__restrict__ col,
                                                      const uint8_t *__restrict__ colors,
                                                      const uint8_t *__restrict__ vclass,
                                                      int32_t *__restrict__ hcnt, int32_t *__restrict__ bcol,
-                                                     int64_t row_begin) {
+                                                     int64_t heavy_min) {
     // rows are local (row_begin + i is the global id); neighbour ids are global.
     // Per warp-row: pass 1 counts colours (lanes of equal colour found by match_any, the
     // lowest lane adds the group size to the warp's shared counter: integer, exact);
@@ -57,16 +60,50 @@ __global__ void __launch_bounds__(256) bucket_kernel(int64_t n, int k, int kp, c
     const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
     for (int64_t i = blockIdx.x * (int64_t)(blockDim.x >> 5) + w; i < n; i += warps) {
         const int64_t e0 = rowptr[i], e1 = rowptr[i + 1];
+        if (e1 - e0 >= heavy_min) continue;  // bucket_heavy_kernel's row
         cnt[lane] = 0;
         __syncwarp();
-        // pass 1 (two chunks in flight)
-        for (int64_t base = e0; base < e1; base += 64) {
-            const int64_t ea = base + lane, eb = base + 32 + lane;
-            const int32_t ja = ea < e1 ? __ldg(col + ea) : -1, jb = eb < e1 ? __ldg(col + eb) : -1;
-            const int ca = ja >= 0 ? (int)colors[ja] : 255, cb = jb >= 0 ? (int)colors[jb] : 255;
-            const unsigned ma = __match_any_sync(0xffffffffu, ca), mb = __match_any_sync(0xffffffffu, cb);
-            if (ca != 255 && (__ffs(ma) - 1) == lane) atomicAdd(&cnt[ca], __popc(ma));
-            if (cb != 255 && (__ffs(mb) - 1) == lane) atomicAdd(&cnt[cb], __popc(mb));
+        // 128 neighbours (4 chunks of 32) in flight per pass; a row of <= 128 neighbours
+        // (~3/4 of RMAT-1M-like rows) is loaded once and placed from registers
+        int32_t jj[4];
+        int cc[4];
+        auto load4 = [&](int64_t base) {
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const int64_t e = base + q * 32 + lane;
+                jj[q] = e < e1 ? __ldg(col + e) : -1;
+            }
+#pragma unroll
+            for (int q = 0; q < 4; ++q) cc[q] = jj[q] >= 0 ? (int)colors[jj[q]] : 255;
+        };
+        auto count4 = [&]() {
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const unsigned m = __match_any_sync(0xffffffffu, cc[q]);
+                if (cc[q] != 255 && (__ffs(m) - 1) == lane) atomicAdd(&cnt[cc[q]], __popc(m));
+            }
+        };
+        auto place4 = [&]() {
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const int c = cc[q];
+                const unsigned m = __match_any_sync(0xffffffffu, c);
+                if (c != 255) {
+                    const int pos = cnt[c] + __popc(m & lanemask_lt());
+                    const int32_t j = jj[q];
+                    bcol[e0 + pos] = tag ? (j | ((int32_t)min((int)vclass[j], 31) << kClassShift)) : j;
+                }
+                __syncwarp();
+                if (c != 255 && (__ffs(m) - 1) == lane) cnt[c] += __popc(m);
+                __syncwarp();
+            }
+        };
+        // pass 1: colour counts (integer adds, exact)
+        load4(e0);
+        count4();
+        for (int64_t base = e0 + 128; base < e1; base += 128) {
+            load4(base);
+            count4();
         }
         __syncwarp();
         const int mine = lane < k ? cnt[lane] : 0;
@@ -81,19 +118,105 @@ __global__ void __launch_bounds__(256) bucket_kernel(int64_t n, int k, int kp, c
         __syncwarp();
         cnt[lane] = incl - mine;  // running write position per colour
         __syncwarp();
-        for (int64_t base = e0; base < e1; base += 32) {
-            const int64_t e = base + lane;
-            const int32_t j = (e < e1) ? __ldg(col + e) : 0;
-            const int c = (e < e1) ? (int)colors[j] : 255;
-            const unsigned m = __match_any_sync(0xffffffffu, c);
-            if (e < e1) {
-                const int pos = cnt[c] + __popc(m & lanemask_lt());
-                bcol[e0 + pos] = tag ? (j | ((int32_t)min((int)vclass[j], 31) << kClassShift)) : j;
+        // pass 2: stable placement (position = running start of the colour + rank among
+        // equal-colour lanes of the chunk)
+        if (e1 - e0 <= 128) {
+            place4();
+        } else {
+            for (int64_t base = e0; base < e1; base += 128) {
+                load4(base);
+                place4();
             }
-            __syncwarp();
-            if (e < e1 && (__ffs(m) - 1) == lane) cnt[c] += __popc(m);
-            __syncwarp();
         }
+    }
+}
+
+// Heavy rows (degree >= 2^kHeavyLog2, rows [0, n_heavy) of the degree order): one CTA
+// per row, so a 56K-neighbour hub is not walked by one warp (it was the whole kernel's
+// critical path).  Same result as bucket_kernel: colour counts (integer adds, exact) and
+// the stable colour-bucketed copy — chunks of 256 neighbours in CSR order, each
+// neighbour's position = its bucket's running start + the counts of its colour in the
+// chunk's earlier warps + its rank among equal-colour lanes of its warp.  Loads of four
+// chunks are in flight together.
+__global__ void __launch_bounds__(256) bucket_heavy_kernel(int64_t n_heavy, int k, int kp, const int64_t *__restrict__ rowptr,
+                                                           const int32_t *__restrict__ col, const uint8_t *__restrict__ colors,
+                                                           const uint8_t *__restrict__ vclass, const int32_t *__restrict__ order,
+                                                           int32_t *__restrict__ hcnt, int32_t *__restrict__ bcol, int64_t nfull) {
+    constexpr int CH = 4;  // chunks of 256 in flight
+    __shared__ int cnt[32];
+    __shared__ int wcnt[8][32];
+    __shared__ int wbase[8][32];
+    __shared__ int run[32];
+    const bool tag = vclass != nullptr && nfull < (int64_t(1) << kClassShift);
+    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+    for (int64_t r = blockIdx.x; r < n_heavy; r += gridDim.x) {
+        const int64_t i = order[r];
+        const int64_t e0 = rowptr[i], e1 = rowptr[i + 1];
+        if (tid < 32) cnt[tid] = 0;
+        __syncthreads();
+        // pass 1: colour counts
+        for (int64_t base = e0; base < e1; base += 256 * CH) {
+            int c[CH];
+#pragma unroll
+            for (int q = 0; q < CH; ++q) {
+                const int64_t e = base + q * 256 + tid;
+                const int32_t j = e < e1 ? __ldg(col + e) : -1;
+                c[q] = j >= 0 ? (int)colors[j] : 255;
+            }
+#pragma unroll
+            for (int q = 0; q < CH; ++q) {
+                const unsigned m = __match_any_sync(0xffffffffu, c[q]);
+                if (c[q] != 255 && (__ffs(m) - 1) == lane) atomicAdd(&cnt[c[q]], __popc(m));
+            }
+        }
+        __syncthreads();
+        if (tid < 32) {
+            const int mine = tid < k ? cnt[tid] : 0;
+            if (tid < kp) hcnt[i * kp + tid] = mine;
+            int incl = mine;
+#pragma unroll
+            for (int off = 1; off < 32; off <<= 1) {
+                const int y = __shfl_up_sync(0xffffffffu, incl, off);
+                if (tid >= off) incl += y;
+            }
+            run[tid] = incl - mine;
+        }
+        __syncthreads();
+        // pass 2: stable placement, CH chunks of loads in flight
+        for (int64_t base = e0; base < e1; base += 256 * CH) {
+            int32_t jj[CH];
+            int c[CH];
+#pragma unroll
+            for (int q = 0; q < CH; ++q) {
+                const int64_t e = base + q * 256 + tid;
+                jj[q] = e < e1 ? __ldg(col + e) : -1;
+                c[q] = jj[q] >= 0 ? (int)colors[jj[q]] : 255;
+            }
+#pragma unroll
+            for (int q = 0; q < CH; ++q) {
+                wcnt[w][lane] = 0;
+                __syncwarp();
+                const unsigned m = __match_any_sync(0xffffffffu, c[q]);
+                const int rank = __popc(m & lanemask_lt());
+                if (c[q] != 255 && (__ffs(m) - 1) == lane) wcnt[w][c[q]] = __popc(m);
+                __syncthreads();
+                if (tid < 32) {  // per colour: exclusive prefix over the 8 warps of the chunk
+                    int s = run[tid];
+#pragma unroll
+                    for (int w2 = 0; w2 < 8; ++w2) {
+                        wbase[w2][tid] = s;
+                        s += wcnt[w2][tid];
+                    }
+                    run[tid] = s;
+                }
+                __syncthreads();
+                if (c[q] != 255) {
+                    const int32_t j = jj[q];
+                    bcol[e0 + wbase[w][c[q]] + rank] = tag ? (j | ((int32_t)min((int)vclass[j], 31) << kClassShift)) : j;
+                }
+            }
+        }
+        __syncthreads();
     }
 }
 
@@ -315,11 +438,10 @@ __device__ __forceinline__ void ema_stage(const AStepArgs &A, T *sBase, const in
                     T *out = reinterpret_cast<T *>(A.msx) + (size_t)iv[v] * A.ldsx;
                     for (int64_t q = t; q < A.ldsx / VN; q += GT) {
                         uint4 w;
+                        int32_t c[VN];  // one aligned vector load of the map (segments padded to 16 B)
+                        load_targets<T>(A.omap, q, c);
 #pragma unroll
-                        for (int el = 0; el < VN; ++el) {
-                            const int32_t c = __ldg(A.omap + q * VN + el);
-                            vset<T>(w, el, c >= 0 ? sB[c] : (T)0);
-                        }
+                        for (int el = 0; el < VN; ++el) vset<T>(w, el, c[el] >= 0 ? sB[c[el]] : (T)0);
                         bad |= nonfinite4<T>(w);
                         __stcs(reinterpret_cast<uint4 *>(out) + q, w);
                     }
@@ -568,8 +690,6 @@ __global__ void __launch_bounds__(256, AStepMinBlocks<U, V, MODE>::value) astep_
 // c ≡ g (mod NG) of each colour bucket, and the NG partial sums are added in a fixed
 // order (g = 0..NG-1) before the push — deterministic, no atomics.  Same stage 2.
 // ---------------------------------------------------------------------------
-static constexpr int kHeavyLog2 = 11;  // rows with >= 2048 neighbours
-
 template <typename T, typename RT, int SG, int R, int U>
 __global__ void __launch_bounds__(256) astep_heavy_kernel(AStepArgs A) {
     constexpr int NG = 256 / SG;
@@ -842,6 +962,427 @@ __global__ void __launch_bounds__(NC + 32, BulkMinBlocks<NC>::value) astep_bulk_
 }
 
 // ---------------------------------------------------------------------------
+// self-fed warp rings (narrow and medium gather rows: u15-1 steps 3-5).  The CTA-wide
+// kernels above spend every neighbour on a block-wide hand-off (mbarrier wait/arrive by
+// every consumer warp, or a group barrier per colour bucket) whose cost does not shrink
+// with the row: at 0.3-1.2 KB per neighbour that overhead, not HBM, set the pace
+// (~100-140 warp instructions per neighbour).  Here a warp owns a row: it is its own
+// producer — up to 32 lanes issue one cp.async.bulk each (the neighbour's plain row or
+// projected segment c(i)) into the warp's ring of S stages — and its own consumer: lane l
+// adds 16-B vectors l, l+32, ... of each staged row into per-colour sums R_x and pushes
+// them into B(i,·) in the warp's shared memory at each colour boundary (a __syncwarp,
+// no block barrier), then runs the shared eMA / top epilogue with a 32-lane group.
+// The issue cursor runs ahead of the consumer across colour buckets AND rows (a queue of
+// the rows it entered), so the ring stays full through row boundaries and epilogues.
+// Rows with >= 2^kHeavyLog2 neighbours (the degree-ordered prefix) are taken first, one
+// row per CTA: warp w takes the neighbours c ≡ w (mod W) of every colour bucket into its
+// own copy of B, and the W copies are added in the fixed order w = 0..W-1 (deterministic,
+// no atomics); light rows are then handed out to warps in chunks (an atomic counter).
+// ---------------------------------------------------------------------------
+static constexpr int kRingQ = 32;      // rows the issue cursor may run ahead of the consumer
+static constexpr int kRingChunk = 4;   // light rows per counter grab
+
+template <int W>
+__device__ __forceinline__ void team_sync() {
+    if constexpr (W == 8) asm volatile("bar.sync 1, 256;" ::: "memory");
+    else asm volatile("bar.sync 1, %0;" ::"n"(W * 32) : "memory");
+}
+
+template <typename T, typename RT, int R, int W>
+__global__ void __launch_bounds__(W * 32) astep_ring_kernel(AStepArgs A, int S, uint32_t stage_bytes, uint32_t warp_bytes,
+                                                            int64_t n_heavy, int *ctr) {
+    constexpr int VN = Vec<T>::N;
+    constexpr int32_t kIdMask = (1 << kClassShift) - 1;
+    extern __shared__ __align__(128) unsigned char smem[];
+    __shared__ RT red[8];
+    __shared__ int s_row;
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    unsigned char *wb = smem + (size_t)w * warp_bytes;
+    uint64_t *full = reinterpret_cast<uint64_t *>(wb);
+    int32_t *rq = reinterpret_cast<int32_t *>(wb + (size_t)S * 8);
+    T *sB = reinterpret_cast<T *>(wb + (((size_t)S * 8 + kRingQ * 4 + 127) / 128) * 128);
+    unsigned char *stages = reinterpret_cast<unsigned char *>(sB) + ((A.smem_group * sizeof(T) + 127) / 128) * 128;
+    const int k = A.k;
+    const int64_t nvec_p = (A.ldseg_p > 0 ? A.ldseg_p : A.ldp) / VN;
+    const uint32_t seg_bytes = (uint32_t)(nvec_p * 16);
+    const size_t row_bytes = (size_t)A.ldp * sizeof(T);
+    const int ls = 31 - __clz(S);  // S is a power of two
+    const uint64_t pol_last = policy_evict_last(), pol_first = A.hint ? policy_evict_first() : policy_evict_normal();
+    if (lane == 0) {
+        for (int q = 0; q < S; ++q) mbar_init(full + q, 1);
+        fence_mbar_init();
+    }
+    __syncthreads();
+
+    // ring counters (warp-uniform): stages issued / consumed, rows entered / consumed
+    uint32_t issued = 0, consumed = 0, q_in = 0, q_out = 0;
+    // issue cursor (warp-uniform; hx: lane x holds the row's count of colour x)
+    int64_t cr = -1, ce = 0, cbase = 0;
+    int cci = 0, cx = k, cleft = 0, chx = 0;
+    int cm = 1, cw = 0;         // member w of m: neighbours c ≡ w (mod m) of each bucket
+    bool cdone = false;         // no more rows for this cursor
+    bool team = false;          // heavy phase: one row, no row queue
+    int64_t chunk = 0;          // light phase: current chunk of rows, position in it
+    int cpos = kRingChunk;
+    int nxt = 0;                // lane 0: the next chunk (counter prefetch)
+
+    // move the cursor to its next row; false when there is none (or the queue is full)
+    auto next_row = [&]() -> bool {
+        if (team || cdone) { cdone = true; return false; }
+        if (q_in - q_out >= (uint32_t)kRingQ) return false;
+        if (cpos == kRingChunk) {
+            chunk = (int64_t)__shfl_sync(0xffffffffu, nxt, 0) * kRingChunk;
+            if (lane == 0) nxt = atomicAdd(ctr + 1, 1);
+            cpos = 0;
+        }
+        const int64_t r = n_heavy + chunk + cpos;
+        if (r >= A.n) { cdone = true; return false; }
+        ++cpos;
+        cr = r;
+        const int64_t i = A.order[r];
+        cci = A.colors[i];
+        cbase = A.rowptr[i];
+        chx = lane < k ? __ldg(A.hcnt + (size_t)i * A.kp + lane) : 0;
+        cx = -1;
+        cleft = 0;
+        if (lane == 0) rq[q_in & (kRingQ - 1)] = (int32_t)r;
+        ++q_in;
+        return true;
+    };
+    // issue up to `budget` stages (warp-uniform)
+    auto issue = [&](int budget) {
+        while (budget > 0) {
+            if (cleft == 0) {
+                // next bucket of a colour != c(i) with neighbours for this member
+                if (cx >= k || cr < 0) {
+                    if (!next_row()) return;
+                }
+                for (;;) {
+                    ++cx;
+                    if (cx >= k) break;
+                    const int c = __shfl_sync(0xffffffffu, chx, cx);
+                    const int64_t b0 = cbase;
+                    cbase += c;
+                    if (cx == cci || c <= cw) continue;
+                    cleft = (c - cw + cm - 1) / cm;
+                    ce = b0 + cw;
+                    break;
+                }
+                if (cx >= k) continue;  // row finished: next row on the next pass
+            }
+            const int take = min(min(cleft, budget), 32);
+            if (lane < take) {
+                const int32_t b = __ldg(A.bcol + ce + (int64_t)lane * cm);
+                const int32_t j = A.tagged ? (b & kIdMask) : b;
+                const uint64_t pol = (A.tagged && (b >> kClassShift) < A.hot_log2) ? pol_last : pol_first;
+                const int rr = cci - (cci > cx ? 1 : 0);
+                const int64_t sbase = A.ldseg_p > 0 ? (int64_t)rr * A.ldseg_p * (int64_t)sizeof(T) : 0;
+                const int slot = (int)((issued + lane) & (uint32_t)(S - 1));
+                mbar_arrive_expect_tx(full + slot, seg_bytes);
+                bulk_g2s(stages + (size_t)slot * stage_bytes, A.mp + (size_t)j * row_bytes + sbase, seg_bytes, full + slot, pol);
+            }
+            issued += take;
+            ce += (int64_t)take * cm;
+            cleft -= take;
+            budget -= take;
+        }
+    };
+    const int refill = S >= 8 ? S / 4 : 1;
+    // gather of one row into sB (this member's neighbours), consuming the ring in order
+    auto gather = [&](int64_t i, int ci, int hx) {
+        for (int x = 0; x < k; ++x) {
+            const int c = __shfl_sync(0xffffffffu, hx, x);
+            if (x == ci || c <= cw) continue;
+            const int cnt = (c - cw + cm - 1) / cm;
+            const int32_t *mp = A.pmap + ((size_t)x * k + ci) * A.cp_map + A.u0;
+            uint4 acc[R];
+            int32_t tt[R][VN];
+#pragma unroll
+            for (int q = 0; q < R; ++q) {
+                acc[q] = make_uint4(0, 0, 0, 0);
+                const int v = lane + q * 32;
+                if (v < nvec_p) load_targets<T>(mp, v, tt[q]);
+            }
+            for (int e = 0; e < cnt; ++e) {
+                const int fr = S - (int)(issued - consumed);
+                if (fr >= refill || issued == consumed) issue(fr);
+                const int slot = (int)(consumed & (uint32_t)(S - 1));
+                mbar_wait(full + slot, (consumed >> ls) & 1u);
+                const unsigned char *st = stages + (size_t)slot * stage_bytes;
+#pragma unroll
+                for (int q = 0; q < R; ++q) {
+                    const int v = lane + q * 32;
+                    if (v < nvec_p) Vec<T>::add(acc[q], lds16(st + (size_t)v * 16));
+                }
+                ++consumed;
+            }
+            // (the lanes' reads of a stage are done before any lane re-issues into it:
+            //  the refill follows this warp's __syncwarp in program order)
+            __syncwarp();
+#pragma unroll
+            for (int q = 0; q < R; ++q) {
+                const int64_t v = lane + q * 32;
+                if (v < nvec_p) {
+#pragma unroll
+                    for (int el = 0; el < VN; ++el)
+                        if (tt[q][el] >= 0 && v * VN + el < A.cp) sB[tt[q][el]] += vget<T>(acc[q], el);
+                }
+            }
+            __syncwarp();  // colours x and x' may push to the same T
+        }
+    };
+
+    bool bad = false;
+    // ---------------- heavy rows: one row per CTA, W members ----------------
+    if (n_heavy > 0) {
+        team = true;
+        cm = W;
+        cw = w;
+        for (;;) {
+            if (threadIdx.x == 0) s_row = atomicAdd(ctr, 1);
+            __syncthreads();
+            const int64_t r = s_row;
+            __syncthreads();
+            if (r >= n_heavy) break;
+            const int64_t i = A.order[r];
+            const int ci = A.colors[i];
+            const int hx = lane < k ? __ldg(A.hcnt + (size_t)i * A.kp + lane) : 0;
+            // cursor on this row only
+            cr = r; cci = ci; cbase = A.rowptr[i]; chx = hx; cx = -1; cleft = 0; cdone = false;
+            for (int64_t q = lane; q < A.ldb / VN; q += 32) reinterpret_cast<uint4 *>(sB)[q] = make_uint4(0, 0, 0, 0);
+            __syncwarp();
+            gather(i, ci, hx);
+            team_sync<W>();
+            // fixed-order sum of the W copies into warp 0's B; M_a staged next to it
+            T *sB0 = reinterpret_cast<T *>(smem + (((size_t)S * 8 + kRingQ * 4 + 127) / 128) * 128);
+            for (int64_t q = threadIdx.x; q < A.ldb / VN; q += W * 32) {
+                uint4 s = reinterpret_cast<const uint4 *>(sB0)[q];
+                for (int w2 = 1; w2 < W; ++w2)
+                    Vec<T>::add(s, reinterpret_cast<const uint4 *>(
+                                       reinterpret_cast<const unsigned char *>(sB0) + (size_t)w2 * warp_bytes)[q]);
+                reinterpret_cast<uint4 *>(sB0)[q] = s;
+            }
+            if (A.comb == COMB_GENERAL && A.stage_a && A.aoff != 0) {
+                const char *a = A.ma + (size_t)i * A.lda * sizeof(T);
+                for (int64_t q = threadIdx.x; q < A.lda / VN; q += W * 32)
+                    reinterpret_cast<uint4 *>(sB0 + A.ldb)[q] = ldg16(a + q * 16);
+            }
+            team_sync<W>();
+            int64_t iv[1] = {i};
+            bool actv[1] = {true};
+            ema_stage<T, RT, W * 32, 1>(A, sB0, iv, actv, threadIdx.x, 0, red, bad);
+            team_sync<W>();
+        }
+        team = false;
+        cdone = false;
+        cm = 1;
+        cw = 0;
+        cr = -1;
+        cx = k;
+        cleft = 0;
+    }
+    // ---------------- light rows: a warp per row ----------------
+    if (lane == 0) nxt = atomicAdd(ctr + 1, 1);
+    for (;;) {
+        if (q_in == q_out) {
+            issue(S - (int)(issued - consumed));
+            if (q_in == q_out) break;
+        }
+        __syncwarp();
+        const int64_t r = rq[q_out & (kRingQ - 1)];
+        ++q_out;
+        const int64_t i = A.order[r];
+        const int ci = A.colors[i];
+        const int hx = lane < k ? __ldg(A.hcnt + (size_t)i * A.kp + lane) : 0;
+        for (int64_t q = lane; q < A.ldb / VN; q += 32) reinterpret_cast<uint4 *>(sB)[q] = make_uint4(0, 0, 0, 0);
+        if (A.comb == COMB_GENERAL && A.stage_a && A.aoff != 0) {
+            const char *a = A.ma + (size_t)i * A.lda * sizeof(T);
+            for (int64_t q = lane; q < A.lda / VN; q += 32) reinterpret_cast<uint4 *>(sB + A.ldb)[q] = ldg16(a + q * 16);
+        }
+        __syncwarp();
+        gather(i, ci, hx);
+        int64_t iv[1] = {i};
+        bool actv[1] = {true};
+        ema_stage<T, RT, 32, 1>(A, sB, iv, actv, lane, w, red, bad);
+        __syncwarp();
+    }
+    if (bad) atomicOr(A.ovf, 1);
+}
+
+// ---------------------------------------------------------------------------
+// warp-per-row register gather across colour buckets (narrow and medium rows).
+// tools/gather_roof.cu measured the TMA engine at ~4.5e9 bulk copies/s per chip, so a
+// bulk copy per neighbour only pays from ~1.5 KB segments; below that, 128-bit loads into
+// registers reach 4.4-6.5 TB/s on random segments.  The register kernels above gather one
+// colour bucket at a time (a group barrier per bucket, ~13 neighbours per bucket on
+// RMAT-1M-like rows, so most loads come from a partly filled tail batch).  Here a warp
+// owns a row and walks the row's live neighbours (its own colour's bucket skipped) as ONE
+// stream in batches of U: the U indices of the next batch are loaded while the current
+// batch's R·U 128-bit loads are in flight, each neighbour's colour comes from a ballot
+// over the bucket ends (lane x holds the end of bucket x), and the per-colour sums R_x
+// are pushed into B(i,·) (warp shared memory, __syncwarp) whenever the colour changes.
+// Rows with >= 2^kHeavyLog2 neighbours are split over the W warps of a CTA (stream
+// elements s ≡ w mod W, private B copies added in the fixed order w = 0..W-1), as in
+// astep_ring_kernel.  Same epilogue (ema_stage).
+// ---------------------------------------------------------------------------
+template <int R, int U>
+struct WrowMinBlocks {
+    static constexpr int value = R <= 2 ? 6 : R == 3 ? 5 : 4;  // 128-thread CTAs (80 / 96 / 128 registers)
+};
+
+template <typename T, typename RT, int R, int U, int W>
+__global__ void __launch_bounds__(W * 32, WrowMinBlocks<R, U>::value) astep_wrow_kernel(AStepArgs A, uint32_t warp_bytes,
+                                                                                       int64_t n_heavy, int *ctr) {
+    constexpr int VN = Vec<T>::N;
+    constexpr int32_t kIdMask = (1 << kClassShift) - 1;
+    extern __shared__ __align__(128) unsigned char smem[];
+    __shared__ RT red[8];
+    __shared__ int s_row;
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    T *sB = reinterpret_cast<T *>(smem + (size_t)w * warp_bytes);
+    const int k = A.k;
+    const int64_t nvec_p = (A.ldseg_p > 0 ? A.ldseg_p : A.ldp) / VN;
+    const size_t row_bytes = (size_t)A.ldp * sizeof(T);
+    const int64_t segb = A.ldseg_p * (int64_t)sizeof(T);
+    const uint64_t pol_last = policy_evict_last(), pol_first = A.hint ? policy_evict_first() : policy_evict_normal();
+    bool bad = false;
+
+    // gather of row i (member mw of mm) into sB
+    auto gather = [&](int64_t i, int ci, int mw, int mm) {
+        const int64_t e0 = A.rowptr[i];
+        const int hx = lane < k ? __ldg(A.hcnt + (size_t)i * A.kp + lane) : 0;
+        int incl = hx;
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, incl, off);
+            if (lane >= off) incl += y;
+        }
+        const int endx = lane < k ? incl : 0x7fffffff;  // end of bucket `lane` (row-relative)
+        const int cnt_ci = __shfl_sync(0xffffffffu, hx, ci);
+        const int sci = __shfl_sync(0xffffffffu, incl, ci) - cnt_ci;
+        const int live = __shfl_sync(0xffffffffu, incl, 31) - cnt_ci;
+        const int len = live > mw ? (live - mw + mm - 1) / mm : 0;  // this member's stream
+        auto pos = [&](int s) { return s < sci ? s : s + cnt_ci; };
+        // indices of batch 0 (lane u < U holds neighbour u of the batch)
+        int32_t bnext = -1;
+        if (lane < U && lane < len) bnext = __ldg(A.bcol + e0 + pos(mw + lane * mm));
+        int curx = -1;
+        uint4 acc[R];
+        int32_t tt[R][VN];
+#pragma unroll
+        for (int q = 0; q < R; ++q) acc[q] = make_uint4(0, 0, 0, 0);
+        auto push = [&]() {
+#pragma unroll
+            for (int q = 0; q < R; ++q) {
+                const int64_t v = lane + q * 32;
+                if (v < nvec_p) {
+#pragma unroll
+                    for (int el = 0; el < VN; ++el)
+                        if (tt[q][el] >= 0 && v * VN + el < A.cp) sB[tt[q][el]] += vget<T>(acc[q], el);
+                }
+                acc[q] = make_uint4(0, 0, 0, 0);
+            }
+            __syncwarp();  // colours x and x' may push to the same T
+        };
+        for (int b0 = 0; b0 < len; b0 += U) {
+            const int32_t bcur = bnext;
+            if (b0 + U < len && lane < U && b0 + U + lane < len) bnext = __ldg(A.bcol + e0 + pos(mw + (b0 + U + lane) * mm));
+            uint4 xv[U][R];
+            int xu[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const bool ok = b0 + u < len;
+                const int32_t b = __shfl_sync(0xffffffffu, bcur, u);
+                const int p = pos(mw + (b0 + u) * mm);
+                xu[u] = ok ? __popc(__ballot_sync(0xffffffffu, endx <= p)) : -1;
+                const int32_t j = A.tagged ? (b & kIdMask) : b;
+                const uint64_t pol = (A.tagged && (b >> kClassShift) < A.hot_log2) ? pol_last : pol_first;
+                const int rr = ci - (ci > xu[u] ? 1 : 0);
+                const char *src = A.mp + (size_t)(ok ? j : 0) * row_bytes + (A.ldseg_p > 0 ? (int64_t)rr * segb : 0) + lane * 16;
+#pragma unroll
+                for (int q = 0; q < R; ++q) xv[u][q] = ldg16_pred(src + q * 512, ok && lane + q * 32 < nvec_p, pol);
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                if (xu[u] < 0) break;
+                if (xu[u] != curx) {
+                    if (curx >= 0) push();
+                    curx = xu[u];
+                    const int32_t *mp = A.pmap + ((size_t)curx * k + ci) * A.cp_map + A.u0;
+#pragma unroll
+                    for (int q = 0; q < R; ++q) {
+                        const int v = lane + q * 32;
+                        if (v < nvec_p) load_targets<T>(mp, v, tt[q]);
+                    }
+                }
+#pragma unroll
+                for (int q = 0; q < R; ++q) Vec<T>::add(acc[q], xv[u][q]);
+            }
+        }
+        if (curx >= 0) push();
+    };
+
+    // ---------------- heavy rows: one row per CTA, W members ----------------
+    if (n_heavy > 0) {
+        for (;;) {
+            if (threadIdx.x == 0) s_row = atomicAdd(ctr, 1);
+            __syncthreads();
+            const int64_t r = s_row;
+            __syncthreads();
+            if (r >= n_heavy) break;
+            const int64_t i = A.order[r];
+            const int ci = A.colors[i];
+            for (int64_t q = lane; q < A.ldb / VN; q += 32) reinterpret_cast<uint4 *>(sB)[q] = make_uint4(0, 0, 0, 0);
+            __syncwarp();
+            gather(i, ci, w, W);
+            team_sync<W>();
+            T *sB0 = reinterpret_cast<T *>(smem);
+            for (int64_t q = threadIdx.x; q < A.ldb / VN; q += W * 32) {
+                uint4 s = reinterpret_cast<const uint4 *>(sB0)[q];
+                for (int w2 = 1; w2 < W; ++w2)
+                    Vec<T>::add(s, reinterpret_cast<const uint4 *>(smem + (size_t)w2 * warp_bytes)[q]);
+                reinterpret_cast<uint4 *>(sB0)[q] = s;
+            }
+            if (A.comb == COMB_GENERAL && A.stage_a && A.aoff != 0) {
+                const char *a = A.ma + (size_t)i * A.lda * sizeof(T);
+                for (int64_t q = threadIdx.x; q < A.lda / VN; q += W * 32)
+                    reinterpret_cast<uint4 *>(sB0 + A.ldb)[q] = ldg16(a + q * 16);
+            }
+            team_sync<W>();
+            int64_t iv[1] = {i};
+            bool actv[1] = {true};
+            ema_stage<T, RT, W * 32, 1>(A, sB0, iv, actv, threadIdx.x, 0, red, bad);
+            team_sync<W>();
+        }
+    }
+    // ---------------- light rows: a warp per row, chunks of rows from a counter ----------------
+    int nxt = lane == 0 ? atomicAdd(ctr + 1, 1) : 0;
+    for (;;) {
+        const int64_t chunk = (int64_t)__shfl_sync(0xffffffffu, nxt, 0) * kRingChunk;
+        if (n_heavy + chunk >= A.n) break;
+        if (lane == 0) nxt = atomicAdd(ctr + 1, 1);  // prefetch the next chunk
+        for (int c = 0; c < kRingChunk; ++c) {
+            const int64_t r = n_heavy + chunk + c;
+            if (r >= A.n) break;
+            const int64_t i = A.order[r];
+            const int ci = A.colors[i];
+            for (int64_t q = lane; q < A.ldb / VN; q += 32) reinterpret_cast<uint4 *>(sB)[q] = make_uint4(0, 0, 0, 0);
+            if (A.comb == COMB_GENERAL && A.stage_a && A.aoff != 0) {
+                const char *a = A.ma + (size_t)i * A.lda * sizeof(T);
+                for (int64_t q = lane; q < A.lda / VN; q += 32) reinterpret_cast<uint4 *>(sB + A.ldb)[q] = ldg16(a + q * 16);
+            }
+            __syncwarp();
+            gather(i, ci, 0, 1);
+            int64_t iv[1] = {i};
+            bool actv[1] = {true};
+            ema_stage<T, RT, 32, 1>(A, sB, iv, actv, lane, w, red, bad);
+            __syncwarp();
+        }
+    }
+    if (bad) atomicOr(A.ovf, 1);
+}
+
+// ---------------------------------------------------------------------------
 // top step, leaf active child: colorful_i = Σ_{j∈N(i), c(j)≠c(i)} M_p(j, topcol[c(j)][c(i)])
 // ---------------------------------------------------------------------------
 // colors: indexed by global vertex id (neighbours); row i's own colour is colors[row_begin + i]
@@ -891,10 +1432,18 @@ int launch_bucket(const Graph &g, const Plan &pl, const uint8_t *colors, int32_t
     if (g.n <= 0) return 0;
     int64_t blocks = std::min<int64_t>((g.n + 7) / 8, (int64_t)num_sms() * 8);
     double bytes = g.nnz * 9.0 + g.nnz * 4.0 + g.n * 16.0 + (double)g.n * pl.kp * 4.0;
+    // heavy rows (a prefix of the degree order) by a CTA each, the rest by a warp each
+    static int heavy = -1;
+    if (heavy < 0) { const char *e = getenv("SG2V_HEAVY"); heavy = e ? atoi(e) : 1; }
+    const int64_t n_heavy = (heavy && g.d_order) ? g.n_deg_ge[kHeavyLog2] : 0;
+    const uint8_t *vcl = g.partitioned ? nullptr : g.d_vclass;
     prof_begin(1, stream);
+    if (n_heavy > 0)
+        bucket_heavy_kernel<<<(unsigned)std::min<int64_t>(n_heavy, (int64_t)num_sms() * 4), 256, 0, (cudaStream_t)stream>>>(
+            n_heavy, pl.k, (int)pl.kp, g.d_rowptr, g.d_col, colors, vcl, g.d_order, hcnt, bcol, g.n);
     bucket_kernel<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(
-        g.n, pl.k, (int)pl.kp, g.d_rowptr, g.d_col, colors, g.partitioned ? nullptr : g.d_vclass, hcnt, bcol,
-        g.row_begin);
+        g.n, pl.k, (int)pl.kp, g.d_rowptr, g.d_col, colors, vcl, hcnt, bcol,
+        n_heavy > 0 ? (int64_t(1) << kHeavyLog2) : (int64_t(1) << 62));
     prof_end(1, bytes, stream);
     return (int)cudaGetLastError();
 }
@@ -948,6 +1497,90 @@ static int launch_astep_bulk_t(const AStepArgs &A, void *stream) {
     if (blocks < 1) blocks = 1;
     kern<<<(unsigned)blocks, kBulkThreads, smem, (cudaStream_t)stream>>>(A, S, stage_bytes);
     return (int)cudaGetLastError();
+}
+
+// Self-fed warp rings (astep_ring_kernel): W = 4 warps per CTA, each with a ring of S
+// (a power of two) stages of ~SG2V_RING_KB (16) KB.
+template <typename T, typename RT, int R>
+static int launch_astep_ring_t(const AStepArgs &A0, void *stream) {
+    constexpr int W = 4;
+    AStepArgs A = A0;
+    // eMA lanes per output for a 32-lane group (GENERAL steps with few outputs)
+    A.tpo = 1;
+    if (A.comb == COMB_GENERAL && !A.top)
+        while (A.tpo < 32 && A.cs * A.tpo * 2 <= 32) A.tpo *= 2;
+    constexpr int VN = Vec<T>::N;
+    const int64_t nvec_p = (A.ldseg_p > 0 ? A.ldseg_p : A.ldp) / VN;
+    const uint32_t stage_bytes = (uint32_t)(nvec_p * 16);
+    static int ring_kb = -1;
+    if (ring_kb < 0) { const char *e = getenv("SG2V_RING_KB"); ring_kb = e ? atoi(e) : 16; }
+    int S = 64;
+    while (S > 2 && (int64_t)S * stage_bytes > (int64_t)ring_kb * 1024) S >>= 1;
+    auto warp_bytes_of = [&](int s) {
+        return (uint32_t)((((size_t)s * 8 + kRingQ * 4 + 127) / 128) * 128 + ((A.smem_group * sizeof(T) + 127) / 128) * 128 +
+                          (((size_t)s * stage_bytes + 127) / 128) * 128);
+    };
+    while (S > 2 && (size_t)W * warp_bytes_of(S) > 220 * 1024) S >>= 1;
+    const uint32_t warp_bytes = warp_bytes_of(S);
+    const size_t smem = (size_t)W * warp_bytes;
+    if (smem > 227 * 1024) return -2;
+    auto kern = astep_ring_kernel<T, RT, R, W>;
+    if (cudaError_t e = ensure_dyn_smem((const void *)kern, smem)) return (int)e;
+    int occ = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, W * 32, smem);
+    if (occ < 1) occ = 1;
+    const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>((A.n + W - 1) / W, (int64_t)occ * num_sms()));
+    int *ctr = A.ovf + 1;  // two scheduling counters next to the overflow flag (workspace)
+    if (cudaError_t e = cudaMemsetAsync(ctr, 0, 2 * sizeof(int), (cudaStream_t)stream)) return (int)e;
+    const int64_t n_heavy = std::min<int64_t>(A.n_heavy, A.n);
+    kern<<<(unsigned)blocks, W * 32, smem, (cudaStream_t)stream>>>(A, S, stage_bytes, warp_bytes, n_heavy, ctr);
+    return (int)cudaGetLastError();
+}
+
+// Warp-per-row register gather (astep_wrow_kernel): W = 4 warps per CTA
+template <typename T, typename RT, int R, int U>
+static int launch_astep_wrow_t(const AStepArgs &A0, void *stream) {
+    constexpr int W = 4;
+    AStepArgs A = A0;
+    A.tpo = 1;  // eMA lanes per output for a 32-lane group (GENERAL steps with few outputs)
+    if (A.comb == COMB_GENERAL && !A.top)
+        while (A.tpo < 32 && A.cs * A.tpo * 2 <= 32) A.tpo *= 2;
+    const uint32_t warp_bytes = (uint32_t)(((A.smem_group * sizeof(T) + 127) / 128) * 128);
+    const size_t smem = (size_t)W * warp_bytes;
+    if (smem > 227 * 1024) return -2;
+    auto kern = astep_wrow_kernel<T, RT, R, U, W>;
+    if (cudaError_t e = ensure_dyn_smem((const void *)kern, smem)) return (int)e;
+    int occ = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, W * 32, smem);
+    if (occ < 1) occ = 1;
+    const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>((A.n + W - 1) / W, (int64_t)occ * num_sms()));
+    int *ctr = A.ovf + 1;  // two scheduling counters next to the overflow flag (workspace)
+    if (cudaError_t e = cudaMemsetAsync(ctr, 0, 2 * sizeof(int), (cudaStream_t)stream)) return (int)e;
+    const int64_t n_heavy = std::min<int64_t>(A.n_heavy, A.n);
+    kern<<<(unsigned)blocks, W * 32, smem, (cudaStream_t)stream>>>(A, warp_bytes, n_heavy, ctr);
+    return (int)cudaGetLastError();
+}
+
+template <typename T, typename RT>
+static int launch_astep_wrow(const AStepArgs &A, int64_t nvec, int ucfg, void *stream) {
+    if (nvec <= 32) {
+        if (ucfg == 4) return launch_astep_wrow_t<T, RT, 1, 4>(A, stream);
+        return launch_astep_wrow_t<T, RT, 1, 8>(A, stream);
+    }
+    if (nvec <= 64) {
+        if (ucfg == 2) return launch_astep_wrow_t<T, RT, 2, 2>(A, stream);
+        return launch_astep_wrow_t<T, RT, 2, 4>(A, stream);
+    }
+    if (nvec <= 96) {
+        if (ucfg == 2) return launch_astep_wrow_t<T, RT, 3, 2>(A, stream);
+        return launch_astep_wrow_t<T, RT, 3, 4>(A, stream);
+    }
+    if (nvec <= 128) return launch_astep_wrow_t<T, RT, 4, 2>(A, stream);
+    if (nvec <= 192) {
+        if (ucfg == 3) return launch_astep_wrow_t<T, RT, 6, 3>(A, stream);
+        return launch_astep_wrow_t<T, RT, 6, 2>(A, stream);
+    }
+    return -2;
 }
 
 // Row-group configuration: narrow rows give every vector of the passive row its own
@@ -1007,6 +1640,44 @@ static int launch_astep_cfg(const AStepArgs &A0, void *stream) {
         bulk = e ? atoi(e) : 1;
         const char *m = getenv("SG2V_BULK_MIN");
         bulk_min = m ? atoi(m) : 64;
+    }
+    // narrow and medium gather rows: warp-per-row register gather across colour buckets
+    // (SG2V_WROW=0 disables; SG2V_WROW_MIN / _MAX: row widths in 16-B vectors; SG2V_WROW_U:
+    // neighbours in flight per batch, among the compiled variants)
+    static int wrow = -1, wrow_min = -1, wrow_max = -1, wrow_u = -1;
+    if (wrow < 0) {
+        const char *e = getenv("SG2V_WROW");
+        wrow = e ? atoi(e) : 1;
+        const char *a = getenv("SG2V_WROW_MIN");
+        wrow_min = a ? atoi(a) : 24;
+        const char *b = getenv("SG2V_WROW_MAX");
+        wrow_max = b ? atoi(b) : 192;
+        const char *u = getenv("SG2V_WROW_U");
+        wrow_u = u ? atoi(u) : 0;
+    }
+    if (MODE == 0 && wrow && !multi && !A.b_out && !A.src_hist && A.pmap != nullptr && nvec >= wrow_min &&
+        nvec <= wrow_max && nvec <= 192) {
+        const int rc = launch_astep_wrow<T, RT>(A, nvec, wrow_u, stream);
+        if (rc != -2) return rc;
+    }
+    // self-fed warp rings of bulk copies (experiments: SG2V_RING=1; SG2V_RING_MAX sets
+    // the widest row in 16-B vectors)
+    static int ring = -1, ring_max = -1;
+    if (ring < 0) {
+        const char *e = getenv("SG2V_RING");
+        ring = e ? atoi(e) : 0;
+        const char *m = getenv("SG2V_RING_MAX");
+        ring_max = m ? atoi(m) : 96;
+    }
+    if (MODE == 0 && ring && !multi && !A.b_out && !A.src_hist && A.pmap != nullptr && nvec <= ring_max && nvec <= 256) {
+        int rc;
+        if (nvec <= 32) rc = launch_astep_ring_t<T, RT, 1>(A, stream);
+        else if (nvec <= 64) rc = launch_astep_ring_t<T, RT, 2>(A, stream);
+        else if (nvec <= 96) rc = launch_astep_ring_t<T, RT, 3>(A, stream);
+        else if (nvec <= 128) rc = launch_astep_ring_t<T, RT, 4>(A, stream);
+        else if (nvec <= 192) rc = launch_astep_ring_t<T, RT, 6>(A, stream);
+        else rc = launch_astep_ring_t<T, RT, 8>(A, stream);
+        if (rc != -2) return rc;
     }
     if (MODE == 0 && bulk && !multi && !A.src_hist && A.pmap != nullptr && nvec >= bulk_min && nvec <= 2048) {
         int rc;
