@@ -1680,14 +1680,29 @@ static int launch_astep_cfg(const AStepArgs &A0, void *stream) {
         if (rc != -2) return rc;
     }
     if (MODE == 0 && bulk && !multi && !A.src_hist && A.pmap != nullptr && nvec >= bulk_min && nvec <= 2048) {
-        int rc;
-        if (nvec <= 64) rc = launch_astep_bulk_t<T, RT, 1, 64>(A, stream);
-        else if (nvec <= 128) rc = launch_astep_bulk_t<T, RT, 1, 128>(A, stream);
-        else if (nvec <= 256) rc = launch_astep_bulk_t<T, RT, 1, 256>(A, stream);
-        else if (nvec <= 512) rc = launch_astep_bulk_t<T, RT, 2, 256>(A, stream);
-        else if (nvec <= 1024) rc = launch_astep_bulk_t<T, RT, 4, 256>(A, stream);
-        else rc = launch_astep_bulk_t<T, RT, 8, 256>(A, stream);
+        auto bulk_launch = [&](const AStepArgs &X) {
+            if (nvec <= 64) return launch_astep_bulk_t<T, RT, 1, 64>(X, stream);
+            if (nvec <= 128) return launch_astep_bulk_t<T, RT, 1, 128>(X, stream);
+            if (nvec <= 256) return launch_astep_bulk_t<T, RT, 1, 256>(X, stream);
+            if (nvec <= 512) return launch_astep_bulk_t<T, RT, 2, 256>(X, stream);
+            if (nvec <= 1024) return launch_astep_bulk_t<T, RT, 4, 256>(X, stream);
+            return launch_astep_bulk_t<T, RT, 8, 256>(X, stream);
+        };
+        int rc = bulk_launch(A);
         if (rc != -2) return rc;  // -2: not a bulk configuration, register gather below
+        // gather-dominated GENERAL steps (few split terms per byte, e.g. u17's 16 = 10 + 6:
+        // 0.025) whose staged M_a row keeps two CTAs from an SM: read M_a through L1 in the
+        // eMA instead and gather with bulk copies (SG2V_UNSTAGE=1; measured slower on u17:
+        // 16 = 10 + 6 922 vs 808 ms, so off by default)
+        static int unstage = -1;
+        if (unstage < 0) { const char *e = getenv("SG2V_UNSTAGE"); unstage = e ? atoi(e) : 0; }
+        if (unstage && A.comb == COMB_GENERAL && A.stage_a && A.aoff != 0 && A.terms_per_byte < vtpb) {
+            AStepArgs B2 = A;
+            B2.stage_a = 0;
+            B2.smem_group = A.ldb;
+            rc = bulk_launch(B2);
+            if (rc != -2) return rc;
+        }
     }
     // heavy rows of narrow register-gather steps: CTA per row first, the rest after
     // (SG2V_HEAVY=0 disables)

@@ -8,4 +8,4 @@ M=gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,lts__t_secto
 timeout 1200 ncu --metrics $M --replay-mode application --clock-control none \
   -k regex:"colorize|bucket|hist|step|top|reduce" --csv --log-file gpurun_out/traffic_${tag}_${t}_${prec}.csv \
   python tools/prof_one.py $t $prec $lay > gpurun_out/traffic_${tag}_${t}_${prec}.log 2>&1
-python tools/traffic_json.py gpurun_out/traffic_${tag}_${t}_${prec}.csv $t $prec $lay 20 --out gpurun_out/ncu_traffic.json
+python tools/traffic_json.py gpurun_out/traffic_${tag}_${t}_${prec}.csv $t $prec $lay 20 --steps gpurun_out/traffic_${tag}_${t}_${prec}.log --out gpurun_out/ncu_traffic.json

@@ -4,8 +4,11 @@
 
 The record is stamped with paper_2009_11665_b200.build.source_hash() of the tree the
 capture ran on; bench.py quotes `traffic` only when the stamp equals its own sources.
-Per class (as bench.py's roofline classes): mean DRAM bytes (read + write) per launch,
-and per launch: kernel, ms, DRAM GB, L2 hit rate.
+Per class (as bench.py's roofline classes): DRAM bytes (read + write) of the class over the
+colouring divided by the class's profiler records (one per DP step, as bench.py counts
+launches: a step may run several kernels — heavy rows, bucket hubs), and per kernel
+launch: kernel, ms, DRAM GB, L2 hit rate.  [--steps LOG]: the prof_one.py log, whose first
+line lists the plan's steps (the last is the top).
 """
 import csv
 import io
@@ -56,9 +59,18 @@ def main():
             c = "top"
         r["cls"] = c
         per.setdefault(c, []).append(r["dram_bytes"])
+    # profiler records per class (bench.py's launch count): one per step
+    nrec = {c: len(v) for c, v in per.items()}
+    if "--steps" in sys.argv:
+        import ast
+        first = open(sys.argv[sys.argv.index("--steps") + 1]).read().splitlines()[0]
+        steps = ast.literal_eval(first)
+        nrec["step"] = len(steps) - 1
+        nrec["top"] = 1
+        nrec["hist"] = 1
     res = json.load(open(out)) if os.path.exists(out) else {}
     res[key] = {"src_hash": source_hash(), "source": os.path.relpath(path, ROOT),
-                "per_class_dram_bytes_per_launch": {c: sum(v) / len(v) for c, v in per.items()},
+                "per_class_dram_bytes_per_launch": {c: sum(v) / max(nrec.get(c, len(v)), 1) for c, v in per.items()},
                 "launches": recs,
                 "how": "ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,"
                        "lts__t_sector_hit_rate.pct --replay-mode application --clock-control none "
