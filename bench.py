@@ -449,6 +449,7 @@ def run_sg2v(args):
         torch.cuda.synchronize()
     prof = sg.profile_read()
     launches_rec = sg.profile_read_launches()
+    n_kernels = sg.profile_kernel_count()  # every kernel of libsg2v launched in the timed region
     sg.profile_enable(False)
     dev_s = ev0.elapsed_time(ev1) / 1e3
     t_max = torch.tensor([dev_s], dtype=torch.float64, device=_dist_device())
@@ -490,8 +491,7 @@ def run_sg2v(args):
 
     # ---- roofline of the dominant kernel class (live CUDA events on the launching stream) ----
     rf, steps_tab, ema = roofline(args, prof, launches_rec, plan)
-    launches = prof["color"]["launches"] + prof["hist"]["launches"] + prof["step"]["launches"] + \
-        prof["top"]["launches"] + 2 * prof["reduce"]["launches"]
+    launches = n_kernels
     clocks = clk.summary()
 
     line = {
@@ -584,6 +584,7 @@ def run_vertex(args):
         ev1.record(stream)
         torch.cuda.synchronize()
     prof = sg.profile_read()
+    n_kernels = sg.profile_kernel_count()  # every kernel of libsg2v launched in the timed region
     sg.profile_enable(False)
     t_max = torch.tensor([ev0.elapsed_time(ev1) / 1e3], dtype=torch.float64, device=_dist_device())
     if world > 1:
@@ -612,7 +613,7 @@ def run_vertex(args):
         peak = float(peaks.get("hbm_gbs", 6650.0))
         dom = "step"
         achieved = prof[dom]["bytes"] / (prof[dom]["ms"] / 1e3) / 1e9 if prof[dom]["ms"] > 0 else 0.0
-        launches = sum(v["launches"] for v in prof.values()) + prof["reduce"]["launches"]
+        launches = n_kernels
         # NVLink: bytes each rank receives per colouring in the whole-row exchange (the
         # plain anchored plan on nl rows: (W-1)·nl·ldp·E per gather step), over the
         # colouring's time — a lower bound on the link rate while exchanging

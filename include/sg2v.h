@@ -290,6 +290,13 @@ sg2v_status sg2v_profile_read(int64_t launches[5], double ms[5], double bytes[5]
 sg2v_status sg2v_profile_read_launches(int64_t cap, int32_t *cls, double *ms, double *alg_bytes,
                                        double *impl_bytes, double *ema_terms, int64_t *n_out);
 
+/* Kernels of this library launched (on any stream, by any thread) since the last
+ * sg2v_profile_enable(1), counted at every launch site — a step may run several
+ * kernels (heavy rows, hub rows of the bucket pass), so this can exceed the
+ * records of sg2v_profile_read_launches.  Counted only while profiling is on;
+ * *n_out must not be NULL (SG2V_EINVAL). */
+sg2v_status sg2v_profile_kernel_count(uint64_t *n_out);
+
 const char *sg2v_last_error(void);
 const char *sg2v_version(void);
 

@@ -5,6 +5,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <atomic>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -91,6 +92,11 @@ static bool g_prof_on = false;
 static std::vector<ProfRec> g_prof;
 static std::vector<cudaEvent_t> g_ev_pool;
 static thread_local cudaEvent_t g_pending = nullptr;
+static std::atomic<uint64_t> g_kernels{0};
+
+void note_launch() {
+    if (g_prof_on) g_kernels.fetch_add(1, std::memory_order_relaxed);
+}
 
 static cudaEvent_t ev_get() {
     if (!g_ev_pool.empty()) {
@@ -1149,7 +1155,17 @@ sg2v_status sg2v_profile_enable(int32_t on) {
     std::lock_guard<std::mutex> lk(g_prof_mu);
     for (auto &r : g_prof) { g_ev_pool.push_back(r.a); g_ev_pool.push_back(r.b); }
     g_prof.clear();
+    g_kernels.store(0);
     g_prof_on = on != 0;
+    return SG2V_OK;
+}
+
+sg2v_status sg2v_profile_kernel_count(uint64_t *n_out) {
+    if (!n_out) {
+        set_error("NULL argument");
+        return SG2V_EINVAL;
+    }
+    *n_out = g_kernels.load();
     return SG2V_OK;
 }
 

@@ -349,6 +349,7 @@ int launch_colorize(uint64_t seed, int64_t j, int64_t n, int k, uint8_t *out, vo
     int64_t blocks = std::min<int64_t>((n + 255) / 256, (int64_t)num_sms() * 16);
     prof_begin(0, stream);
     colorize_kernel<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(seed, j, n, k, out, ids);
+    note_launch();
     prof_end(0, (double)n, stream);
     return (int)cudaGetLastError();
 }
@@ -364,6 +365,7 @@ int launch_hist(const Graph &g, const Plan &pl, const uint8_t *colors, void *H, 
         hist_kernel<double><<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(g.n, pl.k, g.d_rowptr, g.d_col, colors, (double *)H, pl.ldh);
     else
         hist_kernel<u64><<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(g.n, pl.k, g.d_rowptr, g.d_col, colors, (u64 *)H, pl.ldh);
+    note_launch();
     prof_end(1, bytes, stream);
     return (int)cudaGetLastError();
 }
@@ -381,6 +383,7 @@ static int launch_step_t(const StepArgs &A, void *stream) {
     int64_t blocks = std::min<int64_t>(nslots, (int64_t)occ * num_sms());
     if (blocks < 1) blocks = 1;
     kern<<<(unsigned)blocks, 256, smem, (cudaStream_t)stream>>>(A);
+    note_launch();
     return (int)cudaGetLastError();
 }
 
@@ -415,6 +418,7 @@ int launch_step(const Graph &g, const Plan &pl, const Step &st, const uint8_t *c
         else
             top_leaf_kernel<u64, u64><<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(
                 g.n, g.d_rowptr, g.d_col, colors, (const u64 *)src, st.ldp, srch, idx, (u64 *)rowval);
+        note_launch();
         prof_end(3, st.alg_bytes, stream, st.impl_bytes, 0.0);
         return (int)cudaGetLastError();
     }
@@ -454,10 +458,14 @@ int launch_reduce(const Plan &pl, int64_t n, const void *rowval, void *partial, 
     prof_begin(4, stream);
     if (pl.prec == SG2V_U64) {
         reduce_partial_kernel<u64><<<kReduceBlocks, 256, 0, (cudaStream_t)stream>>>((const u64 *)rowval, n, (u64 *)partial);
+        note_launch();
         reduce_final_kernel<u64><<<1, 256, 0, (cudaStream_t)stream>>>((const u64 *)partial, kReduceBlocks, (u64 *)result);
+        note_launch();
     } else {
         reduce_partial_kernel<double><<<kReduceBlocks, 256, 0, (cudaStream_t)stream>>>((const double *)rowval, n, (double *)partial);
+        note_launch();
         reduce_final_kernel<double><<<1, 256, 0, (cudaStream_t)stream>>>((const double *)partial, kReduceBlocks, (double *)result);
+        note_launch();
     }
     prof_end(4, (double)n * 8.0, stream);
     return (int)cudaGetLastError();
@@ -475,11 +483,13 @@ int graph_build_order(Graph &g, void *stream) {
     deg_sorted = deg + n;
     ids = deg + 2 * n;
     degree_kernel<<<(unsigned)std::min<int64_t>((n + 255) / 256, 4096), 256, 0, s>>>(n, g.d_rowptr, deg, ids);
+    note_launch();
     cub::DeviceRadixSort::SortPairsDescending(nullptr, tmp_bytes, deg, deg_sorted, ids, g.d_order, (int)n, 0, 32, s);
     e = cudaMallocAsync(&tmp, tmp_bytes, s);
     if (e == cudaSuccess) {
         cub::DeviceRadixSort::SortPairsDescending(tmp, tmp_bytes, deg, deg_sorted, ids, g.d_order, (int)n, 0, 32, s);
         vclass_kernel<<<(unsigned)std::min<int64_t>((n + 255) / 256, 4096), 256, 0, s>>>(n, g.d_order, g.d_vclass);
+        note_launch();
         int32_t mx = 0;
         cudaMemcpyAsync(&mx, deg_sorted, sizeof(int32_t), cudaMemcpyDeviceToHost, s);
         cudaFreeAsync(tmp, s);
@@ -489,6 +499,7 @@ int graph_build_order(Graph &g, void *stream) {
         int64_t *d_cnt = nullptr;
         if (e == cudaSuccess && (e = cudaMallocAsync((void **)&d_cnt, 32 * sizeof(int64_t), s)) == cudaSuccess) {
             deg_count_kernel<<<1, 32, 0, s>>>(deg_sorted, n, d_cnt);
+            note_launch();
             cudaMemcpyAsync(g.n_deg_ge, d_cnt, 32 * sizeof(int64_t), cudaMemcpyDeviceToHost, s);
             cudaFreeAsync(d_cnt, s);
             e = cudaStreamSynchronize(s);
@@ -505,8 +516,10 @@ int graph_validate(const Graph &g, int *bad, void *stream) {
     cudaError_t e = cudaMalloc(&d_bad, sizeof(int));
     if (e != cudaSuccess) return (int)e;
     cudaMemsetAsync(d_bad, 0, sizeof(int), s);
-    if (g.n > 0)
+    if (g.n > 0) {
         validate_kernel<<<(unsigned)std::min<int64_t>((g.n + 255) / 256, 8192), 256, 0, s>>>(g.n, g.nnz, g.d_rowptr, g.d_col, d_bad);
+        note_launch();
+    }
     cudaMemcpyAsync(bad, d_bad, sizeof(int), cudaMemcpyDeviceToHost, s);
     e = cudaStreamSynchronize(s);
     cudaFree(d_bad);

@@ -202,5 +202,6 @@ int graph_validate(const Graph &g, int *bad, void *stream);
 void prof_begin(int cls, void *stream);
 // alg: SURVEY §8(d) bytes of the launch; impl: the implemented layout's bytes; terms: eMA terms
 void prof_end(int cls, double alg, void *stream, double impl = -1.0, double terms = 0.0);
+void note_launch();  // one kernel of this library launched (sg2v_profile_kernel_count)
 
 }  // namespace sg2v

@@ -56,7 +56,8 @@ SYMBOLS = ["sg2v_graph_load_csr", "sg2v_graph_free", "sg2v_template_build", "sg2
            "sg2v_profile_read", "sg2v_last_error", "sg2v_version", "sg2v_count_batch",
            "sg2v_workspace_bytes_batch", "sg2v_comm_unique_id", "sg2v_comm_init_nccl", "sg2v_comm_init_callback",
            "sg2v_comm_free", "sg2v_graph_load_partition", "sg2v_estimate",
-           "sg2v_profile_read_launches", "sg2v_partition_relabel", "sg2v_graph_set_vertex_ids"]
+           "sg2v_profile_read_launches", "sg2v_partition_relabel", "sg2v_graph_set_vertex_ids",
+           "sg2v_profile_kernel_count"]
 
 ALLGATHER_FN = ctypes.CFUNCTYPE(ctypes.c_int32, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_uint64, ctypes.c_void_p)
 
@@ -101,6 +102,7 @@ def lib():
         L.sg2v_graph_set_vertex_ids.argtypes = [vp, vp, i64]
         L.sg2v_profile_enable.argtypes = [i32]
         L.sg2v_profile_read.argtypes = [vp, vp, vp]
+        L.sg2v_profile_kernel_count.argtypes = [P(u64)]
         L.sg2v_last_error.restype = ctypes.c_char_p
         L.sg2v_version.restype = ctypes.c_char_p
         for name in ("sg2v_graph_load_csr", "sg2v_template_build", "sg2v_template_info", "sg2v_set_options",
@@ -109,7 +111,7 @@ def lib():
                      "sg2v_count_batch", "sg2v_workspace_bytes_batch", "sg2v_comm_unique_id",
                      "sg2v_comm_init_nccl", "sg2v_comm_init_callback", "sg2v_graph_load_partition",
                      "sg2v_estimate", "sg2v_profile_read_launches", "sg2v_partition_relabel",
-                     "sg2v_graph_set_vertex_ids"):
+                     "sg2v_graph_set_vertex_ids", "sg2v_profile_kernel_count"):
             getattr(L, name).restype = ctypes.c_int
         _lib = L
     return _lib
@@ -513,6 +515,13 @@ def profile_read_launches():
                                             te.ctypes.data, ctypes.byref(n)))
     return [{"cls": KERNEL_CLASSES[int(cls[q])], "ms": float(ms[q]), "alg_bytes": float(ab[q]),
              "impl_bytes": float(ib[q]), "ema_terms": float(te[q])} for q in range(m)]
+
+
+def profile_kernel_count() -> int:
+    """Kernels of libsg2v launched since profile_enable(True) (every launch site counted)."""
+    n = ctypes.c_uint64()
+    _check(lib().sg2v_profile_kernel_count(ctypes.byref(n)))
+    return int(n.value)
 
 
 def version() -> str:
