@@ -8,5 +8,5 @@ from .sg2v import (  # noqa: F401
     workspace_bytes_batch, Comm, graph_load_partition, partition_rows,
     graph_load_csr, plan_describe, plan_describe_n, profile_enable, profile_read, template_build,
     workspace_bytes, version, lib, estimate, profile_read_launches, partition_relabel,
-    graph_set_vertex_ids,
+    graph_set_vertex_ids, profile_kernel_count,
 )

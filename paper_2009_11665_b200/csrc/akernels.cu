@@ -576,17 +576,25 @@ __device__ __forceinline__ void ema_stage(const AStepArgs &A, T *sBase, const in
 #ifndef XP_MINB8
 #define XP_MINB8 4  // CTAs per SM of the U = 8 single-row variants (experiments: -DXP_MINB8=5)
 #endif
-template <int U, int V, int MODE>
+template <int U, int V, int MODE, int GT = 256>
 struct AStepMinBlocks {
-    static constexpr int value = V == 1 ? (U >= 16 ? XP_MINB16 : XP_MINB8) : 2;
+    static constexpr int value = GT > 256 ? 1 : V == 1 ? (U >= 16 ? XP_MINB16 : XP_MINB8) : 2;
+};
+
+// CTA size: 256 threads, or one 512-thread group (GT = 512: V-row eMA steps whose V rows
+// take more shared memory than two 256-thread CTAs can share, so the SM's one CTA
+// brings 16 warps instead of 8 to hide the split-table and shared-memory latencies)
+template <int GT>
+struct AStepThreads {
+    static constexpr int value = GT > 256 ? GT : 256;
 };
 
 template <typename T, typename RT, int GT, int R, int U, int V, int MODE>
-__global__ void __launch_bounds__(256, AStepMinBlocks<U, V, MODE>::value) astep_kernel(AStepArgs A) {
-    constexpr int G = 256 / GT;
+__global__ void __launch_bounds__(AStepThreads<GT>::value, AStepMinBlocks<U, V, MODE, GT>::value) astep_kernel(AStepArgs A) {
+    constexpr int G = AStepThreads<GT>::value / GT;
     constexpr int VN = Vec<T>::N;
     extern __shared__ __align__(16) unsigned char smem[];
-    __shared__ RT red[8];
+    __shared__ RT red[AStepThreads<GT>::value / 32];
     const int g = threadIdx.x / GT, t = threadIdx.x % GT;
     T *sBase = reinterpret_cast<T *>(smem) + (size_t)g * V * A.smem_group;
     const int64_t per_slot = (int64_t)G * V;
@@ -1457,17 +1465,18 @@ int launch_bucket(const Graph &g, const Plan &pl, const uint8_t *colors, int32_t
 template <typename T, typename RT, int GT, int R, int U, int V = 1, int MODE = 0>
 static int launch_astep_t(const AStepArgs &A, void *stream) {
     auto kern = astep_kernel<T, RT, GT, R, U, V, MODE>;
-    constexpr int G = 256 / GT;
+    constexpr int NT = AStepThreads<GT>::value;
+    constexpr int G = NT / GT;
     size_t smem = (size_t)G * V * A.smem_group * sizeof(T);
     if (smem > 227 * 1024) return -1;
     if (cudaError_t e = ensure_dyn_smem((const void *)kern, smem)) return (int)e;
     int occ = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 256, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, NT, smem);
     if (occ < 1) occ = 1;
     int64_t nslots = (A.n + (int64_t)G * V - 1) / ((int64_t)G * V);
     int64_t blocks = std::min<int64_t>(nslots, (int64_t)occ * num_sms());
     if (blocks < 1) blocks = 1;
-    kern<<<(unsigned)blocks, 256, smem, (cudaStream_t)stream>>>(A);
+    kern<<<(unsigned)blocks, NT, smem, (cudaStream_t)stream>>>(A);
     note_launch();
     return (int)cudaGetLastError();
 }
@@ -1625,7 +1634,12 @@ static int launch_astep_cfg(const AStepArgs &A0, void *stream) {
     // (a projected output row is written by the same lanes in more passes: the group
     // is sized by the gather and the eMA, not by the k-1 output segments)
     const int64_t nout = std::max(A.ldb, A.ocols) / VN;
-    int64_t want = std::max<int64_t>(nvec, (nout + 3) / 4);
+    // SG2V_GTDIV (experiments, default 4): the epilogue's share of the group width,
+    // want = max(gather vectors, output vectors / GTDIV); a large value sizes narrow
+    // groups by the gather alone (no idle lanes in the gather, longer epilogue loops)
+    static int gtdiv = -1;
+    if (gtdiv < 0) { const char *e = getenv("SG2V_GTDIV"); gtdiv = e ? std::max(1, atoi(e)) : 4; }
+    int64_t want = std::max<int64_t>(nvec, (nout + gtdiv - 1) / gtdiv);
     int gt = 4;
     while (gt < want && gt < 256) gt *= 2;
     if (nvec > 256) gt = 256;
@@ -1634,6 +1648,8 @@ static int launch_astep_cfg(const AStepArgs &A0, void *stream) {
     if (A.comb == COMB_GENERAL && !A.top && gt >= 32)
         while (A.tpo < 32 && A.cs * A.tpo * 2 <= gt) A.tpo *= 2;
     // eMA-heavy GENERAL steps: V = 4 rows share every split-table load
+    static int ema512 = -1;  // SG2V_EMA512=0: V-row eMA CTAs of 256 threads only
+    if (ema512 < 0) { const char *e = getenv("SG2V_EMA512"); ema512 = e ? atoi(e) : 1; }
     static double vtpb = -1;  // SG2V_VTPB (experiments): the terms-per-byte threshold
     if (vtpb < 0) { const char *e = getenv("SG2V_VTPB"); vtpb = e ? atof(e) : 0.05; }
     // (only where the eMA is a real share of the step: >= 0.05 split terms per gathered
@@ -1730,6 +1746,9 @@ static int launch_astep_cfg(const AStepArgs &A0, void *stream) {
     if constexpr (MODE != 0) {
         if constexpr (MODE == 2) {
             if (multi) {
+                // V = 4 rows alone on the SM (> ~113 KB): one 512-thread CTA (SG2V_EMA512=0: 256)
+                if (ema512 && (size_t)4 * A.smem_group * sizeof(T) > 113 * 1024)
+                    return launch_astep_t<T, RT, 512, 1, 8, 4, MODE>(A, stream);
                 if (nvec > 256) return launch_astep_t<T, RT, 256, 1, 16, 4, MODE>(A, stream);
                 return launch_astep_t<T, RT, 256, 1, 8, 4, MODE>(A, stream);
             }
@@ -1740,6 +1759,9 @@ static int launch_astep_cfg(const AStepArgs &A0, void *stream) {
     if (multi) {
         // V = 4 rows per group while they fit in ~100 KB (two CTAs per SM), else V = 2
         const size_t per4 = (size_t)(256 / gt) * 4 * A.smem_group * sizeof(T);
+        // V = 4 rows that only fit one CTA per SM: a 512-thread group (16 warps)
+        if (ema512 && gt == 256 && per4 > 113 * 1024 && per4 <= 200 * 1024 && tune != 6)
+            return launch_astep_t<T, RT, 512, 1, 8, 4>(A, stream);
         if (nvec > 256) {
             if (per4 > 100 * 1024 && tune != 6) return launch_astep_t<T, RT, 256, 1, 16, 2>(A, stream);
             return launch_astep_t<T, RT, 256, 1, 16, 4>(A, stream);

@@ -79,17 +79,16 @@ def want(oracle):
     return {}
 
 
-@pytest.mark.parametrize("cfg", CONFIGS, ids=[",".join(f"{a}={b}" for a, b in d.items()) or "default" for d in CONFIGS])
-def test_ring_gather_vs_oracle(oracle, want, tmp_path, cfg):
+def _run(oracle, want, tmp_path, cfg, names):
     g = hub_graph()
     assert (np.diff(g.row_offsets) >= 2048).sum() >= 4
     f = tmp_path / "rows.npz"
     env = dict(os.environ, **cfg)
-    p = subprocess.run([sys.executable, "-c", _SCRIPT, ",".join(NAMES), str(f)], cwd=ROOT, env=env,
+    p = subprocess.run([sys.executable, "-c", _SCRIPT, ",".join(names), str(f)], cwd=ROOT, env=env,
                        capture_output=True, text=True, timeout=900)
     assert p.returncode == 0, p.stderr[-3000:]
     got = np.load(f)
-    for name in NAMES:
+    for name in names:
         e = TEMPLATES[name]
         k = 1 + max(max(x) for x in e)
         cols = oracle.colors(SEED, J, g.n, k)
@@ -104,3 +103,16 @@ def test_ring_gather_vs_oracle(oracle, want, tmp_path, cfg):
             assert np.array_equal(r, rows), (cfg, name, layout, np.flatnonzero(r != rows)[:10])
             f32 = float(got[f"{name}__{layout}__f32"][0])
             assert math.isclose(f32, f64, rel_tol=1e-4), (cfg, name, layout, f32, f64)
+
+
+@pytest.mark.parametrize("cfg", CONFIGS, ids=[",".join(f"{a}={b}" for a, b in d.items()) or "default" for d in CONFIGS])
+def test_ring_gather_vs_oracle(oracle, want, tmp_path, cfg):
+    _run(oracle, want, tmp_path, cfg, NAMES)
+
+
+# eMA-heavy GENERAL steps whose V = 4 interleaved rows fill the SM's shared memory (U64 /
+# F64 rows of u17's 10 = 5 + 5: 198 KB) run as one 512-thread CTA; SG2V_EMA512=0 keeps the
+# 256-thread CTA.  SG2V_SPLIT=0: the same steps fused (gather + V-row eMA in one kernel).
+@pytest.mark.parametrize("cfg", [{}, {"SG2V_EMA512": "0"}, {"SG2V_SPLIT": "0"}], ids=["default", "ema256", "fused"])
+def test_vrow_ema_512_vs_oracle(oracle, want, tmp_path, cfg):
+    _run(oracle, want, tmp_path, cfg, ("u17", "u16-2"))
