@@ -1634,12 +1634,19 @@ static int launch_astep_cfg(const AStepArgs &A0, void *stream) {
     // (a projected output row is written by the same lanes in more passes: the group
     // is sized by the gather and the eMA, not by the k-1 output segments)
     const int64_t nout = std::max(A.ldb, A.ocols) / VN;
-    // SG2V_GTDIV (experiments, default 4): the epilogue's share of the group width,
-    // want = max(gather vectors, output vectors / GTDIV); a large value sizes narrow
-    // groups by the gather alone (no idle lanes in the gather, longer epilogue loops)
+    // Row-group width: the gather's vectors, widened for the epilogue only on eMA-heavy
+    // GENERAL steps (>= SG2V_VTPB split terms per byte: the V-row eMA wants >= 32 lanes).
+    // Sizing narrow groups by the gather alone leaves no idle lanes in the gather, which
+    // dominates those steps (measured: u17 4 = 2 + 2 32.3 -> 7.6 ms, u15-1 step 3 7.6 ->
+    // 5.1 ms).  SG2V_GTDIV (experiments): want = max(gather vectors, output vectors /
+    // GTDIV) on the other steps too (4 = the previous sizing).
     static int gtdiv = -1;
-    if (gtdiv < 0) { const char *e = getenv("SG2V_GTDIV"); gtdiv = e ? std::max(1, atoi(e)) : 4; }
-    int64_t want = std::max<int64_t>(nvec, (nout + gtdiv - 1) / gtdiv);
+    if (gtdiv < 0) { const char *e = getenv("SG2V_GTDIV"); gtdiv = e ? std::max(1, atoi(e)) : 1 << 20; }
+    static double vtpb0 = -1;
+    if (vtpb0 < 0) { const char *e = getenv("SG2V_VTPB"); vtpb0 = e ? atof(e) : 0.05; }
+    const bool ema_heavy = A.comb == COMB_GENERAL && !A.top && A.terms_per_byte >= vtpb0;
+    const int64_t div = ema_heavy ? 4 : gtdiv;
+    int64_t want = std::max<int64_t>(nvec, (nout + div - 1) / div);
     int gt = 4;
     while (gt < want && gt < 256) gt *= 2;
     if (nvec > 256) gt = 256;
