@@ -1241,7 +1241,13 @@ struct WrowMinBlocks {
     static constexpr int value = R <= 2 ? 6 : R == 3 ? 5 : 4;  // 128-thread CTAs (80 / 96 / 128 registers)
 };
 
-template <typename T, typename RT, int R, int U, int W>
+// NVP > 0: narrow rows (<= NVP <= 16 vectors): lane = (slot, vector), P = 32/NVP slots each
+// take one neighbour per load, so a warp load covers P neighbours; the row is gathered a
+// colour bucket at a time (rounds of P·U neighbours, indices loaded coalesced once per
+// round), the slots' sums added by shuffles at the bucket's end and pushed by slot 0 —
+// the eMA / stores then use all 32 lanes (the register row groups size one group for both,
+// leaving gather lanes idle on narrow-gather GENERAL steps: u14-2's 5 = 3 + 2 ran 4 of 64).
+template <typename T, typename RT, int R, int U, int W, int NVP = 0>
 __global__ void __launch_bounds__(W * 32, WrowMinBlocks<R, U>::value) astep_wrow_kernel(AStepArgs A, uint32_t warp_bytes,
                                                                                        int64_t n_heavy, int *ctr) {
     constexpr int VN = Vec<T>::N;
@@ -1332,6 +1338,59 @@ __global__ void __launch_bounds__(W * 32, WrowMinBlocks<R, U>::value) astep_wrow
         }
         if (curx >= 0) push();
     };
+    // narrow rows: P slots of NVP lanes, a colour bucket at a time (NVP > 0)
+    auto gather_narrow = [&](int64_t i, int ci, int mw, int mm) {
+        constexpr int NV = NVP > 0 ? NVP : 1;
+        constexpr int P = 32 / NV;
+        constexpr int PU = P * U <= 32 ? P * U : 32;
+        const int slot = lane / NV, v = lane % NV;
+        const int64_t e0 = A.rowptr[i];
+        const int hx = lane < k ? __ldg(A.hcnt + (size_t)i * A.kp + lane) : 0;
+        int64_t eb = e0;
+        for (int x = 0; x < k; ++x) {
+            const int c = __shfl_sync(0xffffffffu, hx, x);
+            const int64_t ex = eb;
+            eb += c;
+            if (x == ci || c <= mw) continue;
+            const int cnt = (c - mw + mm - 1) / mm;  // this member's neighbours: mw, mw+mm, ...
+            const int32_t *mp = A.pmap + ((size_t)x * k + ci) * A.cp_map + A.u0;
+            int32_t tt[VN];
+            if (v < nvec_p) load_targets<T>(mp, v, tt);
+            const int rr = ci - (ci > x ? 1 : 0);
+            const char *base = A.mp + (A.ldseg_p > 0 ? (int64_t)rr * segb : 0) + v * 16;
+            uint4 acc = make_uint4(0, 0, 0, 0);
+            for (int c0 = 0; c0 < cnt; c0 += PU) {
+                const int take = min(cnt - c0, PU);
+                const int32_t b = lane < take ? __ldg(A.bcol + ex + mw + (int64_t)(c0 + lane) * mm) : -1;
+                uint4 xv[PU / P];
+#pragma unroll
+                for (int u = 0; u < PU / P; ++u) {
+                    const int32_t bj = __shfl_sync(0xffffffffu, b, u * P + slot);
+                    const int32_t j = A.tagged ? (bj & kIdMask) : bj;
+                    const uint64_t pol = (A.tagged && (bj >> kClassShift) < A.hot_log2) ? pol_last : pol_first;
+                    xv[u] = ldg16_pred(base + (size_t)(bj >= 0 ? j : 0) * row_bytes, bj >= 0 && v < nvec_p, pol);
+                }
+#pragma unroll
+                for (int u = 0; u < PU / P; ++u) Vec<T>::add(acc, xv[u]);
+            }
+            // slots' partial sums (fixed butterfly order: deterministic)
+#pragma unroll
+            for (int off = NV; off < 32; off <<= 1) {
+                uint4 o;
+                o.x = __shfl_xor_sync(0xffffffffu, acc.x, off);
+                o.y = __shfl_xor_sync(0xffffffffu, acc.y, off);
+                o.z = __shfl_xor_sync(0xffffffffu, acc.z, off);
+                o.w = __shfl_xor_sync(0xffffffffu, acc.w, off);
+                Vec<T>::add(acc, o);
+            }
+            if (slot == 0 && v < nvec_p) {
+#pragma unroll
+                for (int el = 0; el < VN; ++el)
+                    if (tt[el] >= 0 && (int64_t)v * VN + el < A.cp) sB[tt[el]] += vget<T>(acc, el);
+            }
+            __syncwarp();  // colours x and x' may push to the same T
+        }
+    };
 
     // ---------------- heavy rows: one row per CTA, W members ----------------
     if (n_heavy > 0) {
@@ -1345,7 +1404,8 @@ __global__ void __launch_bounds__(W * 32, WrowMinBlocks<R, U>::value) astep_wrow
             const int ci = A.colors[i];
             for (int64_t q = lane; q < A.ldb / VN; q += 32) reinterpret_cast<uint4 *>(sB)[q] = make_uint4(0, 0, 0, 0);
             __syncwarp();
-            gather(i, ci, w, W);
+            if constexpr (NVP > 0) gather_narrow(i, ci, w, W);
+            else gather(i, ci, w, W);
             team_sync<W>();
             T *sB0 = reinterpret_cast<T *>(smem);
             for (int64_t q = threadIdx.x; q < A.ldb / VN; q += W * 32) {
@@ -1383,7 +1443,8 @@ __global__ void __launch_bounds__(W * 32, WrowMinBlocks<R, U>::value) astep_wrow
                 for (int64_t q = lane; q < A.lda / VN; q += 32) reinterpret_cast<uint4 *>(sB + A.ldb)[q] = ldg16(a + q * 16);
             }
             __syncwarp();
-            gather(i, ci, 0, 1);
+            if constexpr (NVP > 0) gather_narrow(i, ci, 0, 1);
+            else gather(i, ci, 0, 1);
             int64_t iv[1] = {i};
             bool actv[1] = {true};
             ema_stage<T, RT, 32, 1>(A, sB, iv, actv, lane, w, red, bad);
@@ -1501,7 +1562,9 @@ static int launch_astep_bulk_t(const AStepArgs &A, void *stream) {
     // one CTA per SM (B + M_a rows too wide for two): the register gather keeps more
     // loads in flight there (u17 16 = 10 + 6: 0.88 s vs 1.10 s bulk, 1.30 s bulk with
     // every stage that fits) -> caller falls back
-    if (smem_of(3) > 110 * 1024) return -2;
+    static int bulk1 = -1;  // SG2V_BULK1=1 (experiments): allow the one-CTA-per-SM configuration
+    if (bulk1 < 0) { const char *e = getenv("SG2V_BULK1"); bulk1 = e ? atoi(e) : 0; }
+    if (smem_of(3) > 110 * 1024 && !bulk1) return -2;
     const size_t smem = smem_of(S);
     if (smem > 227 * 1024) return -1;
     auto kern = astep_bulk_kernel<T, RT, R, NC>;
@@ -1556,7 +1619,7 @@ static int launch_astep_ring_t(const AStepArgs &A0, void *stream) {
 }
 
 // Warp-per-row register gather (astep_wrow_kernel): W = 4 warps per CTA
-template <typename T, typename RT, int R, int U>
+template <typename T, typename RT, int R, int U, int NVP = 0>
 static int launch_astep_wrow_t(const AStepArgs &A0, void *stream) {
     constexpr int W = 4;
     AStepArgs A = A0;
@@ -1566,7 +1629,7 @@ static int launch_astep_wrow_t(const AStepArgs &A0, void *stream) {
     const uint32_t warp_bytes = (uint32_t)(((A.smem_group * sizeof(T) + 127) / 128) * 128);
     const size_t smem = (size_t)W * warp_bytes;
     if (smem > 227 * 1024) return -2;
-    auto kern = astep_wrow_kernel<T, RT, R, U, W>;
+    auto kern = astep_wrow_kernel<T, RT, R, U, W, NVP>;
     if (cudaError_t e = ensure_dyn_smem((const void *)kern, smem)) return (int)e;
     int occ = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, W * 32, smem);
@@ -1582,6 +1645,11 @@ static int launch_astep_wrow_t(const AStepArgs &A0, void *stream) {
 
 template <typename T, typename RT>
 static int launch_astep_wrow(const AStepArgs &A, int64_t nvec, int ucfg, void *stream) {
+    // narrow rows: lane-packed slots (U = 32 / P neighbours per round: one index load each)
+    if (nvec <= 2) return launch_astep_wrow_t<T, RT, 1, 2, 2>(A, stream);
+    if (nvec <= 4) return launch_astep_wrow_t<T, RT, 1, 4, 4>(A, stream);
+    if (nvec <= 8) return launch_astep_wrow_t<T, RT, 1, 8, 8>(A, stream);
+    if (nvec <= 16) return launch_astep_wrow_t<T, RT, 1, 8, 16>(A, stream);
     if (nvec <= 32) {
         if (ucfg == 4) return launch_astep_wrow_t<T, RT, 1, 4>(A, stream);
         return launch_astep_wrow_t<T, RT, 1, 8>(A, stream);
@@ -1644,7 +1712,7 @@ static int launch_astep_cfg(const AStepArgs &A0, void *stream) {
     if (gtdiv < 0) { const char *e = getenv("SG2V_GTDIV"); gtdiv = e ? std::max(1, atoi(e)) : 1 << 20; }
     static double vtpb0 = -1;
     if (vtpb0 < 0) { const char *e = getenv("SG2V_VTPB"); vtpb0 = e ? atof(e) : 0.05; }
-    const bool ema_heavy = A.comb == COMB_GENERAL && !A.top && A.terms_per_byte >= vtpb0;
+    const bool ema_heavy = A.comb == COMB_GENERAL && !A.top && A.terms_per_byte >= vtpb0 && A.nterms >= 8;
     const int64_t div = ema_heavy ? 4 : gtdiv;
     int64_t want = std::max<int64_t>(nvec, (nout + div - 1) / div);
     int gt = 4;
@@ -1688,8 +1756,14 @@ static int launch_astep_cfg(const AStepArgs &A0, void *stream) {
         const char *u = getenv("SG2V_WROW_U");
         wrow_u = u ? atoi(u) : 0;
     }
-    if (MODE == 0 && wrow && !multi && !A.b_out && !A.src_hist && A.pmap != nullptr && nvec >= wrow_min &&
-        nvec <= wrow_max && nvec <= 192) {
+    // SG2V_NARROW=1 (experiments): lane-packed warp rows for rows of <= 16 vectors.  Measured
+    // slower than gather-sized register row groups on the 64-B steps (u15-1 step 3 6.2 vs
+    // 4.9 ms, u12-1 5.5 vs 3.7, Orkut u12-1 12.9 vs 7.2: a bucket at a time, its latency is
+    // exposed per bucket), faster on u13-2's step 4 (11.8 vs 13.0 ms): off by default.
+    static int narrow = -1;
+    if (narrow < 0) { const char *e = getenv("SG2V_NARROW"); narrow = e ? atoi(e) : 0; }
+    if (MODE == 0 && wrow && !multi && !A.b_out && !A.src_hist && A.pmap != nullptr &&
+        ((narrow && nvec <= 16) || (nvec >= wrow_min && nvec <= wrow_max && nvec <= 192))) {
         const int rc = launch_astep_wrow<T, RT>(A, nvec, wrow_u, stream);
         if (rc != -2) return rc;
     }

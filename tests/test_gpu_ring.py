@@ -69,7 +69,7 @@ np.savez(sys.argv[2], **{k.replace("/", "__"): v for k, v in out.items()})
 CONFIGS = [{}, {"SG2V_WROW_MIN": "1"}, {"SG2V_WROW_U": "2"}, {"SG2V_WROW_U": "4"}, {"SG2V_WROW_U": "3"},
            {"SG2V_WROW": "0", "SG2V_RING": "1"}, {"SG2V_WROW": "0", "SG2V_RING": "1", "SG2V_RING_KB": "1"},
            {"SG2V_WROW": "0", "SG2V_RING": "1", "SG2V_RING_MAX": "256", "SG2V_RING_KB": "2"},
-           {"SG2V_WROW": "0"}, {"SG2V_WROW": "0", "SG2V_HEAVY": "0"}]
+           {"SG2V_WROW": "0"}, {"SG2V_WROW": "0", "SG2V_HEAVY": "0"}, {"SG2V_NARROW": "0"}]
 
 
 @pytest.fixture(scope="module")

@@ -1,5 +1,6 @@
 """Small runs of every kernel path for compute-sanitizer (memcheck / racecheck / synccheck):
-register and bulk-staged gathers (SG2V_BULK_MIN=1 forces the bulk kernel onto narrow rows too),
+register, warp-row and bulk-staged gathers (SG2V_BULK_MIN=1 forces the bulk kernel onto narrow rows too,
+SG2V_RING=1 the bulk-copy warp rings), 512-thread V-row eMA (u17 in U64),
 CTA-per-heavy-row, V-row eMA, the split eMA pipeline, dense layout, vertex mode (tiles and
 whole rows, world 1).  Checks U64 counts against the oracle so a silent corruption fails too."""
 import os
@@ -22,7 +23,7 @@ graphs = {"hub": csr_from_edges(n, u, v), "er": erdos_renyi(1500, 7000, seed=3)}
 bad = 0
 for gname, g in graphs.items():
     G = sg.graph_load_csr(g.n, g.row_offsets, g.col_indices, validate=True)
-    for name in ("u5-2", "u7-2", "u12-1", "u13-2", "u15-1"):
+    for name in ("u5-2", "u7-2", "u12-1", "u13-2", "u15-1", "u17"):
         e = TEMPLATES[name]
         k = 1 + max(max(x) for x in e)
         want = O.count(g, k, e, O.colors(2, 0, g.n, k))
