@@ -14,6 +14,7 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIBDIR = os.path.join(PKG, "lib")
 LIB = os.path.join(LIBDIR, "libsg2v.so")
+CHECK_LIB = os.path.join(LIBDIR, "libsg2v_check.so")  # device bounds checks (SG2V_DASSERT), tests only
 SOURCES = ["api.cpp", "planner.cpp", "kernels.cu", "akernels.cu"]
 HEADERS = ["sg2v_internal.h", "kcommon.cuh", os.path.join("..", "..", "include", "sg2v.h")]
 
@@ -36,25 +37,28 @@ def source_hash() -> str:
     return h.hexdigest()[:16]
 
 
-def _stale() -> bool:
-    if not os.path.exists(LIB):
+def _stale(lib: str = LIB) -> bool:
+    if not os.path.exists(lib):
         return True
-    t = os.path.getmtime(LIB)
+    t = os.path.getmtime(lib)
     deps = [os.path.join(CSRC, s) for s in SOURCES + HEADERS] + [__file__]
     return any(os.path.getmtime(d) > t for d in deps if os.path.exists(d))
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not _stale():
-        return LIB
+def build(force: bool = False, verbose: bool = False, check: bool = False) -> str:
+    """check=True builds lib/libsg2v_check.so with the device bounds checks compiled in
+    (-DSG2V_CHECK); select it with SG2V_LIB for a test run."""
+    out = CHECK_LIB if check else LIB
+    if not force and not _stale(out):
+        return out
     os.makedirs(LIBDIR, exist_ok=True)
     cuda_lib = "/usr/local/cuda/lib64"
     common = [nvcc(), "-O3", "-std=c++17", "-Xcompiler", "-fPIC,-O3",
               "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo",
-              "-I", os.path.join(ROOT, "include")]
+              "-I", os.path.join(ROOT, "include")] + (["-DSG2V_CHECK"] if check else [])
     if verbose:
         common.insert(1, "-Xptxas=-v")
-    objdir = os.path.join(LIBDIR, "obj")
+    objdir = os.path.join(LIBDIR, "obj_check" if check else "obj")
     os.makedirs(objdir, exist_ok=True)
     objs, procs = [], []
     for s in SOURCES:  # one nvcc per translation unit, in parallel
@@ -68,10 +72,10 @@ def build(force: bool = False, verbose: bool = False) -> str:
         if pr.wait() != 0:
             raise subprocess.CalledProcessError(pr.returncode, cmd)
     link = [nvcc(), "-shared", "-gencode", "arch=compute_100a,code=sm_100a", "-cudart", "shared",
-            "-Xlinker", f"-rpath,{cuda_lib}", "-ldl", "-o", LIB] + objs
+            "-Xlinker", f"-rpath,{cuda_lib}", "-ldl", "-o", out] + objs
     subprocess.check_call(link)
-    return LIB
+    return out
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))
+    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv, check="--check" in sys.argv))

@@ -91,6 +91,7 @@ __global__ void __launch_bounds__(256) bucket_kernel(int64_t n, int k, int kp, c
                 if (c != 255) {
                     const int pos = cnt[c] + __popc(m & lanemask_lt());
                     const int32_t j = jj[q];
+                    SG2V_DASSERT(pos >= 0 && pos < e1 - e0);
                     bcol[e0 + pos] = tag ? (j | ((int32_t)min((int)vclass[j], 31) << kClassShift)) : j;
                 }
                 __syncwarp();
@@ -212,6 +213,7 @@ __global__ void __launch_bounds__(256) bucket_heavy_kernel(int64_t n_heavy, int 
                 __syncthreads();
                 if (c[q] != 255) {
                     const int32_t j = jj[q];
+                    SG2V_DASSERT(wbase[w][c[q]] + rank >= 0 && wbase[w][c[q]] + rank < e1 - e0);
                     bcol[e0 + wbase[w][c[q]] + rank] = tag ? (j | ((int32_t)min((int)vclass[j], 31) << kClassShift)) : j;
                 }
             }
@@ -400,8 +402,10 @@ __device__ __forceinline__ void gather_row(const AStepArgs &A, int64_t i, int ci
 #pragma unroll
                         for (int el = 0; el < VN; ++el)  // (u < cp: a column tile's last vector
                                                           //  may run into the next tile)
-                            if (tt[q][el] >= 0 && (v0 + q * GT + t) * VN + el < A.cp)
+                            if (tt[q][el] >= 0 && (v0 + q * GT + t) * VN + el < A.cp) {
+                                SG2V_DASSERT(A.tile_mode || tt[q][el] < A.ldb);
                                 sB[(size_t)tt[q][el] * STRIDE] += vget<T>(acc[q], el);
+                            }
                     }
                 }
             }
@@ -469,6 +473,7 @@ __device__ __forceinline__ void ema_stage(const AStepArgs &A, T *sBase, const in
                     for (int w = l; w < nt; w += tpo) {
                         const uint32_t q = __ldg(p + w * cs);
                         const uint32_t ia = (q & 0xffffu) + (uint32_t)A.aoff, ib = q >> 16;
+                        SG2V_DASSERT(ia < (uint32_t)A.smem_group && ib < (uint32_t)A.ldb);
                         const uint4 *pa = reinterpret_cast<const uint4 *>(sBase + (size_t)ia * V);
                         const uint4 *pb = reinterpret_cast<const uint4 *>(sBase + (size_t)ib * V);
 #pragma unroll
@@ -774,7 +779,10 @@ __global__ void __launch_bounds__(256) astep_heavy_kernel(AStepArgs A) {
                     for (int g2 = 1; g2 < NG; ++g2) Vec<T>::add(sum, scratch[(size_t)g2 * SG * R + q * SG + ll]);
 #pragma unroll
                     for (int el = 0; el < VN; ++el)
-                        if (tt[el] >= 0 && v * VN + el < A.cp) sB[tt[el]] += vget<T>(sum, el);
+                        if (tt[el] >= 0 && v * VN + el < A.cp) {
+                            SG2V_DASSERT(tt[el] < A.ldb);
+                            sB[tt[el]] += vget<T>(sum, el);
+                        }
                 }
                 group_sync<256>(0);
             }
@@ -956,7 +964,10 @@ __global__ void __launch_bounds__(NC + 32, BulkMinBlocks<NC>::value) astep_bulk_
                 if (v < nvec_p) {
 #pragma unroll
                     for (int el = 0; el < VN; ++el)
-                        if (tt[q][el] >= 0 && v * VN + el < A.cp) sB[tt[q][el]] += vget<T>(acc[q], el);
+                        if (tt[q][el] >= 0 && v * VN + el < A.cp) {
+                            SG2V_DASSERT(tt[q][el] < A.ldb);
+                            sB[tt[q][el]] += vget<T>(acc[q], el);
+                        }
                 }
             }
             group_sync<kBulkConsumers>(0);  // colours x and x' may push to the same T
@@ -1118,6 +1129,7 @@ __global__ void __launch_bounds__(W * 32) astep_ring_kernel(AStepArgs A, int S, 
                 const int fr = S - (int)(issued - consumed);
                 if (fr >= refill || issued == consumed) issue(fr);
                 const int slot = (int)(consumed & (uint32_t)(S - 1));
+                SG2V_DASSERT(issued != consumed && issued - consumed <= (uint32_t)S);
                 mbar_wait(full + slot, (consumed >> ls) & 1u);
                 const unsigned char *st = stages + (size_t)slot * stage_bytes;
 #pragma unroll
@@ -1136,7 +1148,10 @@ __global__ void __launch_bounds__(W * 32) astep_ring_kernel(AStepArgs A, int S, 
                 if (v < nvec_p) {
 #pragma unroll
                     for (int el = 0; el < VN; ++el)
-                        if (tt[q][el] >= 0 && v * VN + el < A.cp) sB[tt[q][el]] += vget<T>(acc[q], el);
+                        if (tt[q][el] >= 0 && v * VN + el < A.cp) {
+                            SG2V_DASSERT(tt[q][el] < A.ldb);
+                            sB[tt[q][el]] += vget<T>(acc[q], el);
+                        }
                 }
             }
             __syncwarp();  // colours x and x' may push to the same T
@@ -1295,7 +1310,10 @@ __global__ void __launch_bounds__(W * 32, WrowMinBlocks<R, U>::value) astep_wrow
                 if (v < nvec_p) {
 #pragma unroll
                     for (int el = 0; el < VN; ++el)
-                        if (tt[q][el] >= 0 && v * VN + el < A.cp) sB[tt[q][el]] += vget<T>(acc[q], el);
+                        if (tt[q][el] >= 0 && v * VN + el < A.cp) {
+                            SG2V_DASSERT(tt[q][el] < A.ldb);
+                            sB[tt[q][el]] += vget<T>(acc[q], el);
+                        }
                 }
                 acc[q] = make_uint4(0, 0, 0, 0);
             }
@@ -1386,7 +1404,10 @@ __global__ void __launch_bounds__(W * 32, WrowMinBlocks<R, U>::value) astep_wrow
             if (slot == 0 && v < nvec_p) {
 #pragma unroll
                 for (int el = 0; el < VN; ++el)
-                    if (tt[el] >= 0 && (int64_t)v * VN + el < A.cp) sB[tt[el]] += vget<T>(acc, el);
+                    if (tt[el] >= 0 && (int64_t)v * VN + el < A.cp) {
+                            SG2V_DASSERT(tt[el] < A.ldb);
+                            sB[tt[el]] += vget<T>(acc, el);
+                        }
             }
             __syncwarp();  // colours x and x' may push to the same T
         }
@@ -1713,10 +1734,13 @@ static int launch_astep_cfg(const AStepArgs &A0, void *stream) {
     static double vtpb0 = -1;
     if (vtpb0 < 0) { const char *e = getenv("SG2V_VTPB"); vtpb0 = e ? atof(e) : 0.05; }
     const bool ema_heavy = A.comb == COMB_GENERAL && !A.top && A.terms_per_byte >= vtpb0 && A.nterms >= 8;
-    const int64_t div = ema_heavy ? 4 : gtdiv;
+    // (a leaf-passive step gathers nothing per neighbour: B = H, its epilogue is the work)
+    const int64_t div = (ema_heavy || A.src_hist) ? 4 : gtdiv;
     int64_t want = std::max<int64_t>(nvec, (nout + div - 1) / div);
     int gt = 4;
     while (gt < want && gt < 256) gt *= 2;
+    // the 256/gt row groups of a CTA must hold their B (+ M_a) rows in shared memory
+    while (gt < 256 && (size_t)(256 / gt) * A.smem_group * sizeof(T) > 160 * 1024) gt *= 2;
     if (nvec > 256) gt = 256;
     // eMA with few outputs: tpo lanes per output (whole warps only)
     A.tpo = 1;

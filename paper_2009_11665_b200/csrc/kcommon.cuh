@@ -4,11 +4,31 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdio>
 #include <map>
 #include <mutex>
 #include <utility>
 
 namespace sg2v {
+
+// Device bounds checks of the check build (libsg2v_check.so, build(check=True)): shared-
+// memory push targets, ring slots, bucket positions.  compute-sanitizer is not available
+// on the GPU pool, so the GPU parity suite is run once against this build as well
+// (tools/check_run.sh); the product build compiles them out.
+#ifdef SG2V_CHECK
+#define SG2V_DASSERT(c)                                                                          \
+    do {                                                                                        \
+        if (!(c)) {                                                                             \
+            printf("SG2V_CHECK failed: %s (%s:%d) block %d thread %d\n", #c, __FILE__, __LINE__, \
+                   (int)blockIdx.x, (int)threadIdx.x);                                          \
+            __trap();                                                                           \
+        }                                                                                       \
+    } while (0)
+#else
+#define SG2V_DASSERT(c) \
+    do {                \
+    } while (0)
+#endif
 
 typedef unsigned long long u64;
 
