@@ -1852,8 +1852,10 @@ static int launch_astep_cfg(const AStepArgs &A0, void *stream) {
         if constexpr (MODE == 2) {
             if (multi) {
                 // V = 4 rows alone on the SM (> ~113 KB): one 512-thread CTA (SG2V_EMA512=0: 256)
-                if (ema512 && (size_t)4 * A.smem_group * sizeof(T) > 113 * 1024)
+                if (ema512 && (size_t)4 * A.smem_group * sizeof(T) > 113 * 1024) {
+                    if (ema512 == 2) return launch_astep_t<T, RT, 1024, 1, 8, 4, MODE>(A, stream);  // (experiment)
                     return launch_astep_t<T, RT, 512, 1, 8, 4, MODE>(A, stream);
+                }
                 if (nvec > 256) return launch_astep_t<T, RT, 256, 1, 16, 4, MODE>(A, stream);
                 return launch_astep_t<T, RT, 256, 1, 8, 4, MODE>(A, stream);
             }
