@@ -1856,6 +1856,10 @@ static int launch_astep_cfg(const AStepArgs &A0, void *stream) {
                     if (ema512 == 2) return launch_astep_t<T, RT, 1024, 1, 8, 4, MODE>(A, stream);  // (experiment)
                     return launch_astep_t<T, RT, 512, 1, 8, 4, MODE>(A, stream);
                 }
+                // (experiment, SG2V_EMA512=3): 8 interleaved rows per 512-thread group, each
+                // split-table load serving 8 rows
+                if (ema512 == 3 && (size_t)8 * A.smem_group * sizeof(T) <= 200 * 1024)
+                    return launch_astep_t<T, RT, 512, 1, 8, 8, MODE>(A, stream);
                 if (nvec > 256) return launch_astep_t<T, RT, 256, 1, 16, 4, MODE>(A, stream);
                 return launch_astep_t<T, RT, 256, 1, 8, 4, MODE>(A, stream);
             }

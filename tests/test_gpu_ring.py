@@ -113,7 +113,7 @@ def test_ring_gather_vs_oracle(oracle, want, tmp_path, cfg):
 # eMA-heavy GENERAL steps whose V = 4 interleaved rows fill the SM's shared memory (U64 /
 # F64 rows of u17's 10 = 5 + 5: 198 KB) run as one 512-thread CTA; SG2V_EMA512=0 keeps the
 # 256-thread CTA.  SG2V_SPLIT=0: the same steps fused (gather + V-row eMA in one kernel).
-@pytest.mark.parametrize("cfg", [{}, {"SG2V_EMA512": "0"}, {"SG2V_EMA512": "2"}, {"SG2V_SPLIT": "0"}],
-                         ids=["default", "ema256", "ema1024", "fused"])
+@pytest.mark.parametrize("cfg", [{}, {"SG2V_EMA512": "0"}, {"SG2V_EMA512": "2"}, {"SG2V_EMA512": "3"}, {"SG2V_SPLIT": "0"}],
+                         ids=["default", "ema256", "ema1024", "emaV8", "fused"])
 def test_vrow_ema_512_vs_oracle(oracle, want, tmp_path, cfg):
     _run(oracle, want, tmp_path, cfg, ("u17", "u16-2"))
