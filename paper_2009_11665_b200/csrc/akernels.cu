@@ -1253,7 +1253,7 @@ __global__ void __launch_bounds__(W * 32) astep_ring_kernel(AStepArgs A, int S, 
 // ---------------------------------------------------------------------------
 template <int R, int U>
 struct WrowMinBlocks {
-    static constexpr int value = R == 1 ? 8 : R == 2 ? 6 : R == 3 ? 5 : 4;  // 128-thread CTAs (64 / 80 / 96 / 128 registers)
+    static constexpr int value = R <= 2 ? 6 : R == 3 ? 5 : 4;  // 128-thread CTAs (80 / 96 / 128 registers)
 };
 
 // NVP > 0: narrow rows (<= NVP <= 16 vectors): lane = (slot, vector), P = 32/NVP slots each
