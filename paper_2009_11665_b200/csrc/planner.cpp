@@ -845,7 +845,10 @@ static void plan_vp_extend(Plan &pl, int64_t n_local, int64_t n_global, int64_t 
     }
     static const int64_t kFullCap = 24ll << 30;  // staging bytes allowed for full rows
     pl.n_global = n_global;
-    pl.vp_full = tile_req <= 0 && n_global * max_ldp * pl.elem <= kFullCap;
+    // (at world 1 the local table is the gather source: no staging, so no cap — the cap
+    //  once sent the Graph500-like scale-22 graph's u15-1 (50 GB of plain rows) to column
+    //  tiles at world 1: 1.92 s instead of ~0.6 s per colouring)
+    pl.vp_full = tile_req <= 0 && (n_global <= n_local || n_global * max_ldp * pl.elem <= kFullCap);
     int64_t off = pl.ws_bytes;
     pl.off_colors_g = off; off = round_up(off + std::max<int64_t>(n_global, 1) + 16, 256);
     if (pl.vp_full) {
