@@ -900,6 +900,32 @@ static sg2v_status count_core(const sg2v_graph *g, const sg2v_template *const *t
             sp.bg = ws + L.off_split;
         }
         const bool anch = pls[0]->layout == LAYOUT_ANCHORED;
+        // colour-grouped row order for the steps gathering exclusion-projected segments of
+        // >= 1 KB: the light rows sorted by c(i) each colouring (launch_colour_order), so the
+        // rows in flight read the same segment of the hub rows; scratch on the call's stream
+        // (SG2V_CORDER=0 disables; measured u15-1 0.565 -> 0.539 s: the top, steps 5-7 read the
+        //  hub rows' segment c(i) while it is hot in L2, ncu-visible as alg frac > 1 on the top)
+        static int corder = -1;
+        if (corder < 0) { const char *e = getenv("SG2V_CORDER"); corder = e ? atoi(e) : 1; }
+        bool any_proj = false;
+        for (Plan *p : pls)
+            for (const Step &stp : p->steps) any_proj = any_proj || (stp.proj_p && stp.ldseg_p * p->elem >= 1024);
+        int32_t *order_c = nullptr;
+        uint8_t *ckeys = nullptr;
+        void *ctmp = nullptr;
+        size_t ctmp_bytes = 0;
+        struct CFree {
+            int32_t *&a; uint8_t *&b; void *&c; cudaStream_t s;
+            ~CFree() { if (a) cudaFreeAsync(a, s); if (b) cudaFreeAsync(b, s); if (c) cudaFreeAsync(c, s); }
+        } cfree{order_c, ckeys, ctmp, s};
+        if (corder && anch && any_proj && g->n > 0) {
+            ctmp_bytes = colour_order_tmp_bytes(g->n);
+            SG2V_CK(cudaMallocAsync((void **)&order_c, g->n * sizeof(int32_t), s));
+            SG2V_CK(cudaMallocAsync((void **)&ckeys, 2 * g->n, s));
+            SG2V_CK(cudaMallocAsync(&ctmp, std::max<size_t>(ctmp_bytes, 16), s));
+        }
+        Graph gco = static_cast<const Graph &>(*g);
+        if (order_c) gco.d_order = order_c;
         bool need_hist = false;
         for (Plan *p : pls) need_hist = need_hist || p->need_hist;
         std::vector<uint64_t> host_ring((size_t)kResultsRing * m);
@@ -911,14 +937,20 @@ static sg2v_status count_core(const sg2v_graph *g, const sg2v_template *const *t
             if (rc) return cuda_fail("colorize", rc);
             if (need_hist && (rc = launch_hist(*g, *pls[0], colors, H, s))) return cuda_fail("hist", rc);
             if (anch && (rc = launch_bucket(*g, *pls[0], colors, hcnt, bcol, s))) return cuda_fail("bucket", rc);
+            if (order_c && (rc = launch_colour_order(*g, colors, order_c, ckeys, ctmp, ctmp_bytes, s)))
+                return cuda_fail("colour order", rc);
             for (int32_t tq = 0; tq < m; ++tq) {
                 const Plan *pl = pls.size() > 1 ? &J.views[tq] : pls[tq];
                 for (const Step &stp : pl->steps) {
+                    // (segments >= 1 KB: narrower segments of many rows read at the same offset
+                    //  measured slower — u15-1 step 4, 320 B: 20.6 -> 23.5 ms)
+                    const bool cgroup = order_c && stp.proj_p && stp.ldseg_p * pl->elem >= 1024;
+                    const Graph &gs = cgroup ? gco : static_cast<const Graph &>(*g);
                     if (anch && stp.split_ema && sp.aux) {
                         sp.rows = pl->split_rows;
-                        rc = launch_astep_split(*g, *pl, stp, colors, hcnt, bcol, ws, rowval, dflag, s, sp);
+                        rc = launch_astep_split(gs, *pl, stp, colors, hcnt, bcol, ws, rowval, dflag, s, sp);
                     } else {
-                        rc = anch ? launch_astep(*g, *pl, stp, colors, hcnt, bcol, ws, rowval, dflag, s)
+                        rc = anch ? launch_astep(gs, *pl, stp, colors, hcnt, bcol, ws, rowval, dflag, s)
                                   : launch_step(*g, *pl, stp, colors, H, ws, rowval, dflag, s);
                     }
                     if (rc == -1) {

@@ -471,6 +471,40 @@ int launch_reduce(const Plan &pl, int64_t n, const void *rowval, void *partial, 
     return (int)cudaGetLastError();
 }
 
+// Colour-grouped processing order (SG2V_CORDER, on): the heavy prefix of the
+// degree order unchanged, the light rows stably sorted by their colour c(i) (degree order
+// kept within a colour), so the CTAs of a wide step gather the SAME segment c(i) of the
+// hub rows at the same time — segment-sized (not row-sized) hot rows for the L2.
+__global__ void colour_keys_kernel(int64_t n, const int32_t *__restrict__ order, const uint8_t *__restrict__ colors,
+                                   uint8_t *__restrict__ keys) {
+    for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n; r += (int64_t)gridDim.x * blockDim.x)
+        keys[r] = colors[order[r]];
+}
+
+size_t colour_order_tmp_bytes(int64_t n) {
+    size_t t = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, t, (const uint8_t *)nullptr, (uint8_t *)nullptr, (const int32_t *)nullptr,
+                                    (int32_t *)nullptr, (int)std::max<int64_t>(n, 1), 0, 8);
+    return t;
+}
+
+int launch_colour_order(const Graph &g, const uint8_t *colors, int32_t *order_out, uint8_t *keys, void *tmp,
+                        size_t tmp_bytes, void *stream) {
+    cudaStream_t s = (cudaStream_t)stream;
+    const int64_t nh = std::min<int64_t>(g.n_deg_ge[11], g.n), nl = g.n - nh;
+    if (nh > 0) {
+        cudaError_t e = cudaMemcpyAsync(order_out, g.d_order, nh * sizeof(int32_t), cudaMemcpyDeviceToDevice, s);
+        if (e != cudaSuccess) return (int)e;
+    }
+    if (nl <= 0) return 0;
+    colour_keys_kernel<<<(unsigned)std::min<int64_t>((nl + 255) / 256, 4096), 256, 0, s>>>(nl, g.d_order + nh, colors, keys);
+    note_launch();
+    cudaError_t e = cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, keys, keys + nl, g.d_order + nh, order_out + nh,
+                                                    (int)nl, 0, 8, s);
+    if (e != cudaSuccess) return (int)e;
+    return (int)cudaGetLastError();
+}
+
 int graph_build_order(Graph &g, void *stream) {
     cudaStream_t s = (cudaStream_t)stream;
     int64_t n = g.n;

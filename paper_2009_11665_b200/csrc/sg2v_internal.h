@@ -196,6 +196,9 @@ int launch_step(const Graph &g, const Plan &pl, const Step &st, const uint8_t *c
 int launch_reduce(const Plan &pl, int64_t n, const void *rowval, void *partial, void *result,
                   void *stream);
 int graph_build_order(Graph &g, void *stream);
+size_t colour_order_tmp_bytes(int64_t n);
+int launch_colour_order(const Graph &g, const uint8_t *colors, int32_t *order_out, uint8_t *keys, void *tmp,
+                        size_t tmp_bytes, void *stream);
 int graph_validate(const Graph &g, int *bad, void *stream);
 
 // profiling (api.cpp)

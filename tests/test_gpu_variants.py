@@ -34,7 +34,7 @@ KNOBS = [
     {"SG2V_BULK": "0"}, {"SG2V_BULK_MIN": "1"}, {"SG2V_BULK_KB": "8"}, {"SG2V_HEAVY": "0"},
     {"SG2V_EMA_SCHED": "1"}, {"SG2V_SPLIT": "0"},
     {"SG2V_GTDIV": "4"}, {"SG2V_GTDIV": "16"}, {"SG2V_EMA512": "0"}, {"SG2V_WROW": "0"}, {"SG2V_WROW_MIN": "1"},
-    {"SG2V_UNSTAGE": "1"}, {"SG2V_NARROW": "0"}, {"SG2V_BULK1": "1"},
+    {"SG2V_UNSTAGE": "1"}, {"SG2V_NARROW": "0"}, {"SG2V_BULK1": "1"}, {"SG2V_CORDER": "0"},
 ]
 
 _SCRIPT = r"""
